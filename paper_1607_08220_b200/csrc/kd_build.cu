@@ -1,0 +1,1414 @@
+// kd_build.cu -- reference-exact kd-tree construction on sm_100a.
+//
+// Reproduces kdknn.local_tree.build_local_tree (local_tree.py:436-574) byte for
+// byte: same split dimension (max sample variance, local_tree.py:111-146), same
+// split value (sampled-histogram approximate median with exact fallback,
+// local_tree.py:147-180 + median.py:74-166), same stable partition
+// (local_tree.py:183-206), same canonical preorder numbering
+// (local_tree.py:320-374) and the same packed bucket order (pack_buckets,
+// local_tree.py:402-405).
+//
+// GPU structure:
+//   breadth-first levels for nodes larger than the sample size (global memory,
+//   SoA coordinates ping-ponged between two buffers):
+//     k_sample   warp/node  exact Fisher-Yates draws, certified variance order,
+//                           sorted unique median sample, 256-boundary window
+//     k_hist     tile/CTA   windowed full-data histogram of the split dim
+//     k_select   warp/node  exact binary64 median selection from the window
+//     k_slow     CTA/node   exact slow path (full histogram, exact fallback,
+//                           next dimensions) -- only for flagged nodes
+//     k_count/scan/k_scatter  stable segmented partition of coords + row ids
+//     k_children thread/node child records, next level, subtree tasks
+//   then one CTA per subtree of <= min(1024, samples) points, built entirely in
+//   shared memory (k_subtree), and a preorder stitch (k_top_* / k_relocate).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "kd_common.cuh"
+#include "kd_tree.cuh"
+#include "kd_warp.cuh"
+
+namespace kdb {
+
+constexpr int MAXS = 1024;       // max sample size supported on device
+constexpr int WIN = 256;         // histogram window (boundaries)
+constexpr int TILE = 4096;       // elements per tile CTA
+constexpr int TILE_THREADS = 256;
+constexpr int SAMPLE_WARPS = 4;
+constexpr int SUB_THREADS = 256;
+constexpr int SUB_WARPS = SUB_THREADS / 32;
+constexpr int SLOW_THREADS = 256;
+constexpr double U64 = 1.1102230246251565e-16;  // 2^-53
+
+enum { ST_SAMPLED = 0, ST_SLOW = 1, ST_LEAF = 2, ST_SPLIT = 3 };
+enum { TS_INTERIOR = 0, TS_TASK = 1 };
+
+struct LNode {
+    int64_t start;
+    int32_t n;
+    int32_t depth;
+    uint64_t path;
+    int32_t slot;
+    uint32_t tile_off;
+};
+
+struct Split {
+    int32_t status;
+    int32_t dim;
+    int32_t nb;
+    int32_t wlo;
+    int32_t whi;
+    int32_t pad;
+    double value;
+    int64_t nl;
+    unsigned long long L;
+};
+
+struct Task {
+    int64_t start;
+    int32_t n;
+    int32_t depth;
+    uint64_t path;
+    int32_t slot;
+    int32_t src;   // which coordinate buffer holds the points
+    int32_t leaf;  // degenerate leaf (all dimensions constant)
+    int32_t pad;
+};
+
+struct DevCtx {
+    int dims;
+    int64_t N;
+    int64_t bucket, ms, vs;
+    uint64_t seed;
+    int ts;  // subtree threshold
+};
+
+template <typename T>
+__device__ __forceinline__ typename KeyOf<T>::type tkey(T v) { return fkey(v); }
+
+// ----------------------------------------------------------------------------
+// certified max-variance dimension (local_tree.py:111-146)
+// fast path: binary64 warp-tree sums with a rigorous bound on the difference to
+// the reference's sequential sums; if the winner is not separated from every
+// other candidate by the bound, the caller recomputes sequentially.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double ssd_bound(double s2, double sabs, int t) {
+    const double tt = (double)t;
+    const double am = sabs / tt;
+    const double dm = (tt + 2.0) * U64 * am;
+    return 4.0 * (tt + 4.0) * U64 * s2 + 2.0 * tt * dm * dm + 1e-300;
+}
+
+// ============================================================================
+// k_sample: one warp per breadth-first node
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(SAMPLE_WARPS * 32)
+k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
+         T* __restrict__ wb, uint32_t* __restrict__ wf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ni = blockIdx.x * SAMPLE_WARPS + warp;
+    if (ni >= K) return;
+    uint64_t* skeys = reinterpret_cast<uint64_t*>(smem_raw) + warp * MAXS;
+    uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * 8) + warp * MAXS;
+    const LNode nd = nodes[ni];
+    const uint32_t n = (uint32_t)nd.n;
+    const int D = c.dims;
+    const int64_t N = c.N;
+
+    // --- variance sample (local_tree.py:122-132)
+    const int take = (int)min((int64_t)n, c.vs);
+    const uint64_t vseed = node_seed(c.seed, nd.path, 0);
+    if (n <= (1u << 22)) fy_resolve<32, uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(skeys), picked);
+    else fy_resolve<32, uint64_t>(n, take, vseed, skeys, picked);
+
+    double s2v[16], eb[16];
+    for (int d = 0; d < D; d++) {
+        const T* row = src + (int64_t)d * N + nd.start;
+        double xs[32];
+        double s1 = 0.0, sa = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; r++) {
+            const int j = r * 32 + lane;
+            xs[r] = j < take ? (double)row[picked[j]] : 0.0;
+            s1 = __dadd_rn(s1, xs[r]);
+            sa = __dadd_rn(sa, fabs(xs[r]));
+        }
+        s1 = warp_sum(s1);
+        sa = warp_sum(sa);
+        const double mean = __ddiv_rn(s1, (double)take);
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; r++) {
+            const int j = r * 32 + lane;
+            if (j < take) {
+                const double df = __dsub_rn(xs[r], mean);
+                s2 = __dadd_rn(s2, __dmul_rn(df, df));
+            }
+        }
+        s2v[d] = warp_sum(s2);
+        eb[d] = ssd_bound(s2v[d], sa, take);
+    }
+    int d0 = 0;
+    for (int d = 1; d < D; d++)
+        if (s2v[d] > s2v[d0]) d0 = d;
+    bool certified = true;
+    for (int d = 0; d < D; d++)
+        if (d != d0 && !(s2v[d0] - s2v[d] > eb[d0] + eb[d])) certified = false;
+    if (!certified) {
+        // exact sequential recomputation in draw order (rare: near-ties)
+        double exact = 0.0;
+        if (lane < D) {
+            const T* row = src + (int64_t)lane * N + nd.start;
+            double mean = 0.0;
+            for (int j = 0; j < take; j++) mean = __dadd_rn(mean, (double)row[picked[j]]);
+            mean = __ddiv_rn(mean, (double)take);
+            double s = 0.0;
+            for (int j = 0; j < take; j++) {
+                const double df = __dsub_rn((double)row[picked[j]], mean);
+                s = __dadd_rn(s, __dmul_rn(df, df));
+            }
+            exact = s;
+        }
+        d0 = 0;
+        double best = __shfl_sync(FULL, exact, 0);
+        for (int d = 1; d < D; d++) {
+            const double e = __shfl_sync(FULL, exact, d);
+            if (-e < -best) { best = e; d0 = d; }  // np.argsort(-ssd, mergesort)[0]
+        }
+    }
+
+    // --- median sample of dim d0 (local_tree.py:149-156)
+    const int m = (int)min((int64_t)n, c.ms);
+    const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
+    __syncwarp();
+    if (n <= (1u << 22)) fy_resolve<32, uint32_t>(n, m, mseed, reinterpret_cast<uint32_t*>(skeys), picked);
+    else fy_resolve<32, uint64_t>(n, m, mseed, skeys, picked);
+    typedef typename KeyOf<T>::type Key;
+    const T* row = src + (int64_t)d0 * N + nd.start;
+    Key kv[32];
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+        const int j = r * 32 + lane;
+        kv[r] = j < m ? tkey(row[picked[j]]) : ~(Key)0;
+    }
+    warp_sort<32>(kv);
+    // np.unique: first element of each run of equal keys; boundary index = rank of run
+    int nb_run = 0, cle = 0;
+    const int mid = m / 2;
+    Split* sp = split + ni;
+    T* wbn = wb + (int64_t)ni * WIN;
+    int bidx[32];
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+        const int s = r * 32 + lane;
+        Key prev = __shfl_up_sync(FULL, kv[r], 1);
+        const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
+        if (lane == 0) prev = lp;
+        const bool first = s < m && (s == 0 || kv[r] != prev);
+        const unsigned bal = __ballot_sync(FULL, first);
+        bidx[r] = first ? nb_run + __popc(bal & ((1u << lane) - 1)) : -1;
+        nb_run += __popc(bal);
+        // boundary (run) containing sorted position `mid`
+        cle += __popc(__ballot_sync(FULL, first && s <= mid));
+    }
+    const int center = cle - 1;
+    const int nb = nb_run;
+    int wlo = max(0, center - WIN / 2);
+    const int whi = min(nb, wlo + WIN);
+    wlo = max(0, whi - WIN);
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+        if (bidx[r] >= wlo && bidx[r] < whi) wbn[bidx[r] - wlo] = key_inv(kv[r], (T*)nullptr);
+    }
+    uint32_t* wfn = wf + (int64_t)ni * WIN;
+    for (int i = lane; i < WIN; i += 32) wfn[i] = 0;
+    if (lane == 0) {
+        sp->status = ST_SAMPLED;
+        sp->dim = d0;
+        sp->nb = nb;
+        sp->wlo = wlo;
+        sp->whi = whi;
+        sp->value = 0.0;
+        sp->nl = 0;
+        sp->L = 0ULL;
+    }
+}
+
+__device__ __forceinline__ int tile_node(const LNode* nodes, int K, uint32_t t) {
+    int lo = 0, hi = K;  // last node with tile_off <= t
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (nodes[mid].tile_off <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// ============================================================================
+// k_hist: windowed histogram (median.py:128-140 restricted to the boundaries
+// around the sampled median; counts below the window are aggregated in L)
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(TILE_THREADS)
+k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
+       const T* __restrict__ wb, uint32_t* __restrict__ wf) {
+    __shared__ T sb[WIN];
+    __shared__ uint32_t sf[WIN];
+    __shared__ unsigned long long sL;
+    const uint32_t t = blockIdx.x;
+    const int ni = tile_node(nodes, K, t);
+    const LNode nd = nodes[ni];
+    const Split sp = split[ni];
+    const int nw = sp.whi - sp.wlo;
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
+        sf[i] = 0;
+        if (i < nw) sb[i] = wb[(int64_t)ni * WIN + i];
+    }
+    if (threadIdx.x == 0) sL = 0;
+    __syncthreads();
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
+    const T* row = src + (int64_t)sp.dim * c.N + nd.start;
+    const T lo_b = sb[0], hi_b = sb[nw - 1];
+    unsigned long long lc = 0;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const T v = row[e];
+        if (v < lo_b) {
+            lc++;
+        } else if (v < hi_b) {
+            int lo = 1, hi = nw - 1;  // upper_bound over the window
+            while (lo < hi) {
+                const int md = (lo + hi) >> 1;
+                if (sb[md] <= v) lo = md + 1; else hi = md;
+            }
+            atomicAdd(&sf[lo], 1u);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
+    if ((threadIdx.x & 31) == 0 && lc) atomicAdd(&sL, lc);
+    __syncthreads();
+    if (threadIdx.x == 0 && sL) atomicAdd(&split[ni].L, sL);
+    for (int i = threadIdx.x + 1; i < nw; i += blockDim.x)
+        if (sf[i]) atomicAdd(&wf[(int64_t)ni * WIN + i], sf[i]);
+}
+
+// ============================================================================
+// k_select: exact binary64 selection (median.py:143-166) from the window
+// ============================================================================
+template <typename T>
+__global__ void k_select(const LNode* __restrict__ nodes, int K, Split* split, const T* __restrict__ wb,
+                         const uint32_t* __restrict__ wf, int* slow_list, int* slow_count) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ni = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (ni >= K) return;
+    Split sp = split[ni];
+    const int64_t n = nodes[ni].n;
+    const int nw = sp.whi - sp.wlo;
+    constexpr int PER = WIN / 32;
+    // lane owns window entries [lane*PER, lane*PER+PER)
+    int64_t loc[PER];
+    int64_t run = 0;
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const int i = lane * PER + q;
+        run += (i >= 1 && i < nw) ? (int64_t)wf[(int64_t)ni * WIN + i] : 0;
+        loc[q] = run;
+    }
+    int64_t excl = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(FULL, excl, o);
+        if (lane >= o) excl += y;
+    }
+    excl -= run;
+    const int64_t L = (int64_t)sp.L;
+    double best = INFINITY;
+    int besti = 0x7fffffff;
+    int64_t bestc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const int i = lane * PER + q;
+        if (i < nw) {
+            const int64_t cum = L + excl + loc[q];
+            const double df = half_diff(cum, n);
+            if (df < best) { best = df; besti = i; bestc = cum; }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FULL, best, o);
+        const int oi = __shfl_xor_sync(FULL, besti, o);
+        const int64_t oc = __shfl_xor_sync(FULL, bestc, o);
+        if (ob < best || (ob == best && oi < besti)) { best = ob; besti = oi; bestc = oc; }
+    }
+    // cum at window ends
+    const int64_t cum_lo = L;
+    int64_t cum_hi = 0;
+    {
+        const int ih = nw - 1;
+        const int owner = ih / PER, q = ih % PER;
+        int64_t mine = 0;
+#pragma unroll
+        for (int qq = 0; qq < PER; qq++)
+            if (qq == q) mine = L + excl + loc[qq];
+        cum_hi = __shfl_sync(FULL, mine, owner);
+    }
+    if (lane == 0) {
+        const double xlo = __ddiv_rn((double)cum_lo, (double)n);
+        const double xhi = __ddiv_rn((double)cum_hi, (double)n);
+        const bool okl = sp.wlo == 0 || (xlo <= 0.5 && besti > 0);
+        const bool okr = sp.whi == sp.nb || xhi >= 0.5;
+        if (okl && okr && bestc > 0 && bestc < n) {
+            sp.status = ST_SPLIT;
+            sp.value = (double)wb[(int64_t)ni * WIN + besti];
+            sp.nl = bestc;
+        } else {
+            sp.status = ST_SLOW;
+            slow_list[atomicAdd(slow_count, 1)] = ni;
+        }
+        split[ni] = sp;
+    }
+}
+
+// ============================================================================
+// k_slow: the reference's full split choice for one node (rare path)
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(SLOW_THREADS)
+k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Split* split,
+       const int* slow_list, const int* slow_count) {
+    typedef typename KeyOf<T>::type Key;
+    __shared__ uint64_t skeys[MAXS];
+    __shared__ uint32_t picked[MAXS];
+    __shared__ T sb[MAXS];
+    __shared__ int hist[MAXS + 1];
+    __shared__ double s2x[16];
+    __shared__ int order[16];
+    __shared__ int s_nb;
+    __shared__ unsigned long long red[SLOW_THREADS / 32];
+    __shared__ Key kred[SLOW_THREADS / 32];
+    __shared__ int s_done;
+    __shared__ double s_val;
+    __shared__ int64_t s_nl;
+    __shared__ int s_dim;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cnt = *slow_count;
+    const int D = c.dims;
+    const int64_t N = c.N;
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+        const int ni = slow_list[li];
+        const LNode nd = nodes[ni];
+        const int64_t n = nd.n;
+        // ---- exact variance order (sequential, draw order)
+        const int take = (int)min(n, c.vs);
+        if (warp == 0) {
+            const uint64_t vseed = node_seed(c.seed, nd.path, 0);
+            if (n <= (1 << 22)) fy_resolve<32, uint32_t>((uint32_t)n, take, vseed, reinterpret_cast<uint32_t*>(skeys), picked);
+            else fy_resolve<32, uint64_t>((uint32_t)n, take, vseed, skeys, picked);
+            if (lane < D) {
+                const T* row = src + (int64_t)lane * N + nd.start;
+                double mean = 0.0;
+                for (int j = 0; j < take; j++) mean = __dadd_rn(mean, (double)row[picked[j]]);
+                mean = __ddiv_rn(mean, (double)take);
+                double s = 0.0;
+                for (int j = 0; j < take; j++) {
+                    const double df = __dsub_rn((double)row[picked[j]], mean);
+                    s = __dadd_rn(s, __dmul_rn(df, df));
+                }
+                s2x[lane] = s;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                for (int d = 0; d < D; d++) order[d] = d;
+                for (int a = 1; a < D; a++) {  // stable insertion sort on -ssd
+                    const int tt = order[a];
+                    int p = a - 1;
+                    while (p >= 0 && -s2x[order[p]] > -s2x[tt]) { order[p + 1] = order[p]; p--; }
+                    order[p + 1] = tt;
+                }
+            }
+        }
+        if (threadIdx.x == 0) s_done = 0;
+        __syncthreads();
+        for (int oi = 0; oi < D; oi++) {
+            const int d = order[oi];
+            const T* row = src + (int64_t)d * N + nd.start;
+            const int m = (int)min(n, c.ms);
+            if (warp == 0) {
+                const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d);
+                if (n <= (1 << 22)) fy_resolve<32, uint32_t>((uint32_t)n, m, mseed, reinterpret_cast<uint32_t*>(skeys), picked);
+                else fy_resolve<32, uint64_t>((uint32_t)n, m, mseed, skeys, picked);
+                Key kv[32];
+#pragma unroll
+                for (int r = 0; r < 32; r++) {
+                    const int j = r * 32 + lane;
+                    kv[r] = j < m ? tkey(row[picked[j]]) : ~(Key)0;
+                }
+                warp_sort<32>(kv);
+                int nbr = 0;
+#pragma unroll
+                for (int r = 0; r < 32; r++) {
+                    const int s = r * 32 + lane;
+                    Key prev = __shfl_up_sync(FULL, kv[r], 1);
+                    const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
+                    if (lane == 0) prev = lp;
+                    const bool first = s < m && (s == 0 || kv[r] != prev);
+                    const unsigned bal = __ballot_sync(FULL, first);
+                    if (first) sb[nbr + __popc(bal & ((1u << lane) - 1))] = key_inv(kv[r], (T*)nullptr);
+                    nbr += __popc(bal);
+                }
+                if (lane == 0) s_nb = nbr;
+            }
+            __syncthreads();
+            const int nb = s_nb;
+            for (int i = threadIdx.x; i <= nb; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+                const T v = row[e];
+                int lo = 0, hi = nb;
+                while (lo < hi) {
+                    const int md = (lo + hi) >> 1;
+                    if (sb[md] <= v) lo = md + 1; else hi = md;
+                }
+                atomicAdd(&hist[lo], 1);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {  // median.py:143-166, sequential
+                int64_t cum = 0, below = 0;
+                int bi = -1;
+                double bd = INFINITY;
+                for (int i = 0; i < nb; i++) {
+                    cum += hist[i];
+                    const double df = half_diff(cum, n);
+                    if (df < bd) { bd = df; bi = i; below = cum; }
+                }
+                if (bi >= 0 && below > 0 && below < n) {
+                    s_done = 1; s_dim = d; s_val = (double)sb[bi]; s_nl = below;
+                }
+            }
+            __syncthreads();
+            if (s_done) break;
+            // ---- exact fallback (local_tree.py:162-177): s = k-th smallest, k = n/2
+            const int64_t kth = n / 2;
+            Key prefix = 0;
+            int64_t krem = kth;
+            constexpr int KB = KeyOf<T>::bits;
+            for (int shift = KB - 8; shift >= 0; shift -= 8) {
+                for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+                __syncthreads();
+                const Key hmask = shift + 8 >= KB ? (Key)0 : (~(Key)0) << (shift + 8);
+                for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+                    const Key k = tkey(row[e]);
+                    if ((k & hmask) == (prefix & hmask)) atomicAdd(&hist[(int)((k >> shift) & 255)], 1);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    int64_t acc = 0;
+                    int dg = 0;
+                    for (; dg < 256; dg++) {
+                        if (acc + hist[dg] > krem) break;
+                        acc += hist[dg];
+                    }
+                    krem -= acc;
+                    s_nb = dg;
+                }
+                __syncthreads();
+                prefix |= ((Key)s_nb) << shift;
+                __syncthreads();
+            }
+            const Key ks = prefix;
+            // below / equal counts and the next distinct value
+            unsigned long long lt = 0, eq = 0;
+            Key nxt = ~(Key)0;
+            for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+                const Key k = tkey(row[e]);
+                lt += k < ks;
+                eq += k == ks;
+                if (k > ks && k < nxt) nxt = k;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                lt += __shfl_xor_sync(FULL, lt, o);
+                eq += __shfl_xor_sync(FULL, eq, o);
+                const Key on = __shfl_xor_sync(FULL, nxt, o);
+                nxt = on < nxt ? on : nxt;
+            }
+            if (lane == 0) { red[warp] = lt | (eq << 32); kred[warp] = nxt; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int64_t below = 0, eqc = 0;
+                Key nx = ~(Key)0;
+                for (int w = 0; w < SLOW_THREADS / 32; w++) {
+                    below += (int64_t)(red[w] & 0xFFFFFFFFULL);
+                    eqc += (int64_t)(red[w] >> 32);
+                    if (kred[w] < nx) nx = kred[w];
+                }
+                const double half = (double)n * 0.5;
+                const int64_t i1 = below, i2 = below + eqc;
+                const bool v1 = i1 >= 1, v2 = i2 < n;
+                if (v1 || v2) {
+                    bool pick2 = !v1 || (v2 && fabs((double)i2 - half) < fabs((double)i1 - half));
+                    s_done = 1;
+                    s_dim = d;
+                    s_val = pick2 ? (double)key_inv(nx, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
+                    s_nl = pick2 ? i2 : i1;
+                }
+            }
+            __syncthreads();
+            if (s_done) break;
+        }
+        if (threadIdx.x == 0) {
+            Split sp = split[ni];
+            if (s_done) {
+                sp.status = ST_SPLIT; sp.dim = s_dim; sp.value = s_val; sp.nl = s_nl;
+            } else {
+                sp.status = ST_LEAF;
+            }
+            split[ni] = sp;
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================
+// stable segmented partition (local_tree.py:183-233), coordinates + row ids
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(TILE_THREADS)
+k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c,
+        const Split* __restrict__ split, uint32_t* tile_left) {
+    __shared__ uint32_t red[TILE_THREADS / 32];
+    const uint32_t t = blockIdx.x;
+    const int ni = tile_node(nodes, K, t);
+    const LNode nd = nodes[ni];
+    const Split sp = split[ni];
+    uint32_t cnt = 0;
+    if (sp.status == ST_SPLIT) {
+        const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
+        const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
+        const T* row = src + (int64_t)sp.dim * c.N + nd.start;
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) cnt += (double)row[e] < sp.value;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < TILE_THREADS / 32; w++) s += red[w];
+        tile_left[t] = s;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TILE_THREADS)
+k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
+          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, int K, DevCtx c,
+          const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff) {
+    __shared__ uint32_t wl[TILE_THREADS / 32];
+    const uint32_t t = blockIdx.x;
+    const int ni = tile_node(nodes, K, t);
+    const LNode nd = nodes[ni];
+    const Split sp = split[ni];
+    if (sp.status != ST_SPLIT) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
+    const uint32_t lbefore = tile_loff[t] - tile_loff[nd.tile_off];  // lefts in earlier tiles of this node
+    int64_t lrun = lbefore;
+    int64_t rrun = e0 - lbefore;
+    const int D = c.dims;
+    const int64_t N = c.N;
+    const T* srow = src + (int64_t)sp.dim * N + nd.start;
+    for (int64_t base = e0; base < e1; base += TILE_THREADS) {
+        const int64_t e = base + threadIdx.x;
+        const bool valid = e < e1;
+        const bool f = valid && (double)srow[e] < sp.value;
+        const unsigned bal = __ballot_sync(FULL, f);
+        const unsigned vbal = __ballot_sync(FULL, valid);
+        if (lane == 0) wl[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t lw = 0, ltot = 0, vw = 0;
+        for (int w = 0; w < TILE_THREADS / 32; w++) {
+            const uint32_t x = wl[w];
+            if (w < warp) lw += x;
+            ltot += x;
+        }
+        (void)vw;
+        const uint32_t lp = lw + __popc(bal & ((1u << lane) - 1));
+        const int64_t chunk_valid = min((int64_t)TILE_THREADS, e1 - base);
+        if (valid) {
+            int64_t pos;
+            if (f) pos = lrun + lp;
+            else pos = sp.nl + rrun + (threadIdx.x - lp);
+            const int64_t gs = nd.start + e, gd = nd.start + pos;
+            for (int d = 0; d < D; d++) dst[(int64_t)d * N + gd] = src[(int64_t)d * N + gs];
+            idst[gd] = isrc[gs];
+        }
+        (void)vbal;
+        lrun += ltot;
+        rrun += chunk_valid - ltot;
+        __syncthreads();
+    }
+}
+
+// ============================================================================
+// k_children: records + next level + subtree tasks
+// ============================================================================
+struct TopStore {
+    int32_t* dim;
+    double* val;
+    int32_t* left;
+    int32_t* right;
+    int32_t* npts;
+    int32_t* kind;
+    int32_t* task;
+    int32_t* nodes;  // subtree node counts
+    int32_t* pre;    // preorder index
+};
+
+__global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* __restrict__ split, DevCtx c,
+                           int dst_parity, int src_parity, int child_base, TopStore ts, LNode* next,
+                           unsigned long long* next_ctr, Task* tasks, int* task_ctr) {
+    const int ni = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ni >= K) return;
+    const LNode nd = nodes[ni];
+    const Split sp = split[ni];
+    if (sp.status == ST_LEAF) {
+        const int t = atomicAdd(task_ctr, 1);
+        tasks[t] = Task{nd.start, nd.n, nd.depth, nd.path, nd.slot, src_parity, 1, 0};
+        ts.kind[nd.slot] = TS_TASK;
+        ts.task[nd.slot] = t;
+        ts.npts[nd.slot] = nd.n;
+        return;
+    }
+    const int ls = child_base + 2 * ni, rs = ls + 1;
+    ts.kind[nd.slot] = TS_INTERIOR;
+    ts.dim[nd.slot] = sp.dim;
+    ts.val[nd.slot] = sp.value;
+    ts.left[nd.slot] = ls;
+    ts.right[nd.slot] = rs;
+    ts.npts[nd.slot] = nd.n;
+    const int64_t cs[2] = {nd.start, nd.start + sp.nl};
+    const int32_t cn[2] = {(int32_t)sp.nl, (int32_t)(nd.n - sp.nl)};
+    const int32_t slot[2] = {ls, rs};
+    const uint64_t cp[2] = {nd.path * 2ULL, nd.path * 2ULL + 1ULL};
+    for (int k = 0; k < 2; k++) {
+        ts.npts[slot[k]] = cn[k];
+        if (cn[k] > c.ts) {
+            const uint32_t nt = (uint32_t)((cn[k] + TILE - 1) / TILE);
+            const unsigned long long old = atomicAdd(next_ctr, (1ULL << 32) | nt);
+            const int idx = (int)(old >> 32);
+            next[idx] = LNode{cs[k], cn[k], nd.depth + 1, cp[k], slot[k], (uint32_t)(old & 0xFFFFFFFFULL)};
+            ts.kind[slot[k]] = TS_INTERIOR;
+        } else {
+            const int t = atomicAdd(task_ctr, 1);
+            tasks[t] = Task{cs[k], cn[k], nd.depth + 1, cp[k], slot[k], dst_parity, 0, 0};
+            ts.kind[slot[k]] = TS_TASK;
+            ts.task[slot[k]] = t;
+        }
+    }
+}
+
+// ============================================================================
+// k_subtree: one CTA builds a whole subtree of <= ts points in shared memory
+// ============================================================================
+struct SubSmem {
+    // sizes (elements) for a given ts, dims, T
+    static __host__ __device__ size_t bytes(int ts, int dims, int tsize) {
+        size_t b = 0;
+        b += (size_t)dims * ts * tsize;  // coords
+        b = (b + 15) & ~size_t(15);
+        b += (size_t)ts * 4;             // orig ids
+        b += (size_t)2 * ts * 2;         // perm ping-pong
+        b = (b + 15) & ~size_t(15);
+        const int ns = 2 * ts + 2;
+        b += (size_t)ns * 8;             // split values (double)
+        b += (size_t)ns * 2 * 5;         // start, cnt, left, right, cnt/pre scratch
+        b += (size_t)ns * 2;             // pre
+        b += (size_t)ns;                 // dim (int8)
+        b = (b + 15) & ~size_t(15);
+        const int nl = ts / 2 + 2;
+        b += (size_t)2 * nl * 8;         // level list paths
+        b += (size_t)2 * nl * 2;         // level list slots
+        b += (size_t)(ts + 2) * 2;       // level starts
+        b = (b + 15) & ~size_t(15);
+        b += (size_t)MAXS * 4 * 2;       // FY scratch (keys + picked)
+        b += 64;
+        return b;
+    }
+};
+
+template <typename T, int R>
+__device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, int ts, int D, uint64_t path,
+                          const DevCtx& c, uint32_t* fykeys, uint32_t* fypicked, int* fylock,
+                          int& out_dim, double& out_val, int& out_nl) {
+    typedef typename KeyOf<T>::type Key;
+    const int lane = threadIdx.x & 31;
+    // per-dim: constant?, fast ssd + bound
+    double s2v[16], eb[16];
+    bool nonconst[16];
+    for (int d = 0; d < D; d++) {
+        const T* row = cs + d * ts;
+        double xs[R];
+        Key kmn = ~(Key)0, kmx = 0;
+        double s1 = 0.0, sa = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int i = r * 32 + lane;
+            if (i < n) {
+                const T v = row[perm[start + i]];
+                xs[r] = (double)v;
+                const Key k = tkey(v);
+                kmn = k < kmn ? k : kmn;
+                kmx = k > kmx ? k : kmx;
+            } else {
+                xs[r] = 0.0;
+            }
+            s1 = __dadd_rn(s1, xs[r]);
+            sa = __dadd_rn(sa, fabs(xs[r]));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const Key a = __shfl_xor_sync(FULL, kmn, o), b = __shfl_xor_sync(FULL, kmx, o);
+            kmn = a < kmn ? a : kmn;
+            kmx = b > kmx ? b : kmx;
+        }
+        nonconst[d] = kmn != kmx;
+        s1 = warp_sum(s1);
+        sa = warp_sum(sa);
+        const double mean = __ddiv_rn(s1, (double)n);
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int i = r * 32 + lane;
+            if (i < n) {
+                const double df = __dsub_rn(xs[r], mean);
+                s2 = __dadd_rn(s2, __dmul_rn(df, df));
+            }
+        }
+        s2v[d] = warp_sum(s2);
+        eb[d] = ssd_bound(s2v[d], sa, n);
+    }
+    int best = -1;
+    for (int d = 0; d < D; d++)
+        if (nonconst[d] && (best < 0 || s2v[d] > s2v[best])) best = d;
+    out_dim = -1;
+    if (best < 0) return;  // every dimension constant: degenerate leaf
+    bool certified = true;
+    for (int d = 0; d < D; d++)
+        if (d != best && nonconst[d] && !(s2v[best] - s2v[d] > eb[best] + eb[d])) certified = false;
+    if (!certified) {
+        // exact: Fisher-Yates order over the node (take == n) and sequential sums
+        if (lane == 0) while (atomicCAS(fylock, 0, 1) != 0) {}
+        __syncwarp();
+        __threadfence_block();
+        fy_resolve<R, uint32_t>((uint32_t)n, n, node_seed(c.seed, path, 0), fykeys, fypicked);
+        double exact = 0.0;
+        if (lane < D) {
+            const T* row = cs + lane * ts;
+            double mean = 0.0;
+            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[perm[start + fypicked[j]]]);
+            mean = __ddiv_rn(mean, (double)n);
+            double s = 0.0;
+            for (int j = 0; j < n; j++) {
+                const double df = __dsub_rn((double)row[perm[start + fypicked[j]]], mean);
+                s = __dadd_rn(s, __dmul_rn(df, df));
+            }
+            exact = s;
+        }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) atomicExch(fylock, 0);
+        // first non-constant dimension in stable descending order
+        best = -1;
+        double bv = 0.0;
+        for (int d = 0; d < D; d++) {
+            const double e = __shfl_sync(FULL, exact, d);
+            if (!nonconst[d]) continue;
+            if (best < 0 || -e < -bv) { best = d; bv = e; }
+        }
+    }
+    // exact median select over all n values (n <= sample size: boundaries = all
+    // distinct values; median.py:143-166 reduces to the two boundaries around n/2)
+    const T* row = cs + best * ts;
+    Key kv[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int i = r * 32 + lane;
+        kv[r] = i < n ? tkey(row[perm[start + i]]) : ~(Key)0;
+    }
+    warp_sort<R>(kv);
+    const Key ks = warp_get<R>(kv, n / 2);
+    int lt = 0, eq = 0;
+    Key nxt = ~(Key)0;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int i = r * 32 + lane;
+        if (i < n) {
+            lt += kv[r] < ks;
+            eq += kv[r] == ks;
+            if (kv[r] > ks && kv[r] < nxt) nxt = kv[r];
+        }
+    }
+    lt = warp_isum(lt);
+    eq = warp_isum(eq);
+    for (int o = 16; o > 0; o >>= 1) {
+        const Key on = __shfl_xor_sync(FULL, nxt, o);
+        nxt = on < nxt ? on : nxt;
+    }
+    const int cumA = lt, cumB = lt + eq;
+    bool pickB;
+    if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
+    else if (cumB >= n) pickB = false;    // no boundary after A
+    else pickB = half_diff(cumB, n) < half_diff(cumA, n);
+    out_dim = best;
+    out_val = pickB ? (double)key_inv(nxt, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
+    out_nl = pickB ? cumB : cumA;
+}
+
+template <typename T>
+__device__ __forceinline__ void sub_split_dispatch(const T* cs, const uint16_t* perm, int start, int n, int ts, int D,
+                                                   uint64_t path, const DevCtx& c, uint32_t* fk, uint32_t* fp,
+                                                   int* lock, int& dim, double& val, int& nl) {
+    if (n <= 32) sub_split<T, 1>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+    else if (n <= 64) sub_split<T, 2>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+    else if (n <= 128) sub_split<T, 4>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+    else if (n <= 256) sub_split<T, 8>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+    else if (n <= 512) sub_split<T, 16>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+    else sub_split<T, 32>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SUB_THREADS)
+k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0, const int32_t* idx1, DevCtx c,
+          KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, int32_t* task_nodes, int32_t* task_depth) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Task tk = tasks[blockIdx.x];
+    const int D = c.dims;
+    const int64_t N = c.N;
+    const int ts = c.ts;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const T* src = tk.src ? buf1 : buf0;
+    const int32_t* isrc = tk.src ? idx1 : idx0;
+    KdNode* out_nodes = scratch + 2 * tk.start;
+    int32_t* out_cnt = scnt + 2 * tk.start;
+
+    if (tk.leaf || tk.n > ts) {
+        // degenerate leaf (possibly larger than the shared-memory limit): copy through
+        if (tk.src) {
+            for (int64_t e = threadIdx.x; e < tk.n; e += blockDim.x) {
+                for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = src[(int64_t)d * N + tk.start + e];
+                idx0[tk.start + e] = isrc[tk.start + e];
+            }
+        }
+        if (threadIdx.x == 0) {
+            out_nodes[0] = KdNode{0.0, (int32_t)tk.start, -1 - tk.n};
+            out_cnt[0] = tk.n;
+            task_nodes[blockIdx.x] = 1;
+            task_depth[blockIdx.x] = tk.depth;
+        }
+        return;
+    }
+    const int n = tk.n;
+    // ---- carve shared memory
+    unsigned char* p = smem_raw;
+    T* cs = reinterpret_cast<T*>(p); p += (size_t)D * ts * sizeof(T);
+    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
+    int32_t* cidx = reinterpret_cast<int32_t*>(p); p += (size_t)ts * 4;
+    uint16_t* perm0 = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
+    uint16_t* perm1 = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
+    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
+    const int NS = 2 * ts + 2;
+    double* nv = reinterpret_cast<double*>(p); p += (size_t)NS * 8;
+    uint16_t* nstart = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    uint16_t* ncnt = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    uint16_t* nleft = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    uint16_t* nright = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    uint16_t* nsub = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    uint16_t* npre = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
+    int8_t* ndim = reinterpret_cast<int8_t*>(p); p += (size_t)NS;
+    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
+    const int NL = ts / 2 + 2;
+    uint64_t* lpath0 = reinterpret_cast<uint64_t*>(p); p += (size_t)NL * 8;
+    uint64_t* lpath1 = reinterpret_cast<uint64_t*>(p); p += (size_t)NL * 8;
+    uint16_t* lslot0 = reinterpret_cast<uint16_t*>(p); p += (size_t)NL * 2;
+    uint16_t* lslot1 = reinterpret_cast<uint16_t*>(p); p += (size_t)NL * 2;
+    uint16_t* lvl = reinterpret_cast<uint16_t*>(p); p += (size_t)(ts + 2) * 2;
+    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
+    uint32_t* fykeys = reinterpret_cast<uint32_t*>(p); p += (size_t)MAXS * 4;
+    uint32_t* fypicked = reinterpret_cast<uint32_t*>(p); p += (size_t)MAXS * 4;
+    int* misc = reinterpret_cast<int*>(p);  // [0]=slots [1]=next count [2]=lock [3]=maxlevel [4]=cur count
+    // ---- load the task's points
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        for (int d = 0; d < D; d++) cs[d * ts + e] = src[(int64_t)d * N + tk.start + e];
+        cidx[e] = isrc[tk.start + e];
+        perm0[e] = (uint16_t)e;
+    }
+    if (threadIdx.x == 0) {
+        misc[0] = 1; misc[1] = 0; misc[2] = 0; misc[3] = 0;
+        nstart[0] = 0; ncnt[0] = (uint16_t)n;
+        lvl[0] = 0; lvl[1] = 1;
+        if (n > c.bucket) { lslot0[0] = 0; lpath0[0] = tk.path; misc[4] = 1; }
+        else { ndim[0] = -1; misc[4] = 0; }
+    }
+    __syncthreads();
+    uint16_t* pc = perm0;
+    uint16_t* pn = perm1;
+    uint64_t* lpc = lpath0; uint64_t* lpn = lpath1;
+    uint16_t* lsc = lslot0; uint16_t* lsn = lslot1;
+    int level = 0;
+    // root leaf: emit
+    if (misc[4] == 0) {
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = cs[d * ts + e];
+            idx0[tk.start + e] = cidx[e];
+        }
+    }
+    while (true) {
+        const int cnt = misc[4];
+        if (cnt == 0) break;
+        for (int li = warp; li < cnt; li += SUB_WARPS) {
+            const int slot = lsc[li];
+            const uint64_t path = lpc[li];
+            const int st = nstart[slot], nn = ncnt[slot];
+            int dim;
+            double val;
+            int nl;
+            sub_split_dispatch<T>(cs, pc, st, nn, ts, D, path, c, fykeys, fypicked, &misc[2], dim, val, nl);
+            if (dim < 0) {  // degenerate leaf
+                if (lane == 0) { ndim[slot] = -1; }
+                for (int e = lane; e < nn; e += 32) {
+                    const int q = pc[st + e];
+                    for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + st + e] = cs[d * ts + q];
+                    idx0[tk.start + st + e] = cidx[q];
+                }
+                continue;
+            }
+            // stable partition pc[st..st+nn) -> pn
+            int lrun = 0;
+            const T* row = cs + dim * ts;
+            for (int b = 0; b < nn; b += 32) {
+                const int e = b + lane;
+                const bool valid = e < nn;
+                const int q = valid ? pc[st + e] : 0;
+                const bool f = valid && (double)row[q] < val;
+                const unsigned bal = __ballot_sync(FULL, f);
+                const int lp = __popc(bal & ((1u << lane) - 1));
+                if (valid) {
+                    const int pos = f ? lrun + lp : nl + (e - (lrun + lp));
+                    pn[st + pos] = (uint16_t)q;
+                }
+                lrun += __popc(bal);
+            }
+            __syncwarp();
+            int cb = 0;
+            if (lane == 0) cb = atomicAdd(&misc[0], 2);
+            cb = __shfl_sync(FULL, cb, 0);
+            if (lane == 0) {
+                ndim[slot] = (int8_t)dim;
+                nv[slot] = val;
+                nleft[slot] = (uint16_t)cb;
+                nright[slot] = (uint16_t)(cb + 1);
+                nstart[cb] = (uint16_t)st; ncnt[cb] = (uint16_t)nl;
+                nstart[cb + 1] = (uint16_t)(st + nl); ncnt[cb + 1] = (uint16_t)(nn - nl);
+            }
+            // children: push or emit
+            for (int k = 0; k < 2; k++) {
+                const int cst = k ? st + nl : st, cn = k ? nn - nl : nl;
+                if (cn > c.bucket) {
+                    if (lane == 0) {
+                        const int q = atomicAdd(&misc[1], 1);
+                        lsn[q] = (uint16_t)(cb + k);
+                        lpn[q] = path * 2ULL + (uint64_t)k;
+                    }
+                } else {
+                    if (lane == 0) ndim[cb + k] = -1;
+                    for (int e = lane; e < cn; e += 32) {
+                        const int q = pn[cst + e];
+                        for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + cst + e] = cs[d * ts + q];
+                        idx0[tk.start + cst + e] = cidx[q];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        level++;
+        if (threadIdx.x == 0) {
+            misc[4] = misc[1];
+            misc[1] = 0;
+            lvl[level + 1] = (uint16_t)misc[0];
+            misc[3] = level;
+        }
+        __syncthreads();
+        { uint16_t* t = pc; pc = pn; pn = t; }
+        { uint64_t* t = lpc; lpc = lpn; lpn = t; }
+        { uint16_t* t = lsc; lsc = lsn; lsn = t; }
+        // nodes of the next level live in (new) pc; ranges of finished nodes are final
+    }
+    // levels: slots [lvl[L], lvl[L+1]) hold depth-L nodes, L in [0, nlev)
+    const int nlev = misc[3] + 1;
+    const int nslots = misc[0];
+    // bottom-up subtree sizes
+    for (int L = nlev - 1; L >= 0; L--) {
+        const int a = lvl[L], b = min((int)lvl[L + 1], nslots);
+        for (int s = a + threadIdx.x; s < b; s += blockDim.x)
+            nsub[s] = ndim[s] < 0 ? 1 : (uint16_t)(1 + nsub[nleft[s]] + nsub[nright[s]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) npre[0] = 0;
+    __syncthreads();
+    for (int L = 0; L < nlev; L++) {
+        const int a = lvl[L], b = min((int)lvl[L + 1], nslots);
+        for (int s = a + threadIdx.x; s < b; s += blockDim.x) {
+            if (ndim[s] >= 0) {
+                npre[nleft[s]] = (uint16_t)(npre[s] + 1);
+                npre[nright[s]] = (uint16_t)(npre[s] + 1 + nsub[nleft[s]]);
+            }
+        }
+        __syncthreads();
+    }
+    // deepest leaf depth: a node at level L has depth tk.depth + L
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+        const int q = npre[s];
+        if (ndim[s] >= 0) out_nodes[q] = KdNode{nv[s], (int32_t)npre[nright[s]], (int32_t)ndim[s]};
+        else out_nodes[q] = KdNode{0.0, (int32_t)(tk.start + nstart[s]), -1 - (int32_t)ncnt[s]};
+        out_cnt[q] = ncnt[s];
+    }
+    if (threadIdx.x == 0) {
+        task_nodes[blockIdx.x] = nsub[0];
+        // depth of the deepest node: last level that holds any slot
+        int L = nlev - 1;
+        while (L > 0 && lvl[L] >= nslots) L--;
+        task_depth[blockIdx.x] = tk.depth + L;
+    }
+}
+
+// ============================================================================
+// preorder stitch of the breadth-first top and the subtree tasks
+// ============================================================================
+__device__ __forceinline__ int child_nodes(const TopStore& ts, const int32_t* task_nodes, int s) {
+    return ts.kind[s] == TS_TASK ? task_nodes[ts.task[s]] : ts.nodes[s];
+}
+
+__global__ void k_top_count(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const int s = lv[i].slot;
+    if (ts.kind[s] != TS_INTERIOR) return;
+    ts.nodes[s] = 1 + child_nodes(ts, task_nodes, ts.left[s]) + child_nodes(ts, task_nodes, ts.right[s]);
+}
+
+__global__ void k_top_pre(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes, int32_t* task_base,
+                          KdNode* nodes, int32_t* ncount) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const int s = lv[i].slot;
+    if (ts.kind[s] != TS_INTERIOR) return;
+    const int p = ts.pre[s];
+    const int l = ts.left[s], r = ts.right[s];
+    const int pl = p + 1, pr = p + 1 + child_nodes(ts, task_nodes, l);
+    ts.pre[l] = pl;
+    ts.pre[r] = pr;
+    if (ts.kind[l] == TS_TASK) task_base[ts.task[l]] = pl;
+    if (ts.kind[r] == TS_TASK) task_base[ts.task[r]] = pr;
+    nodes[p] = KdNode{ts.val[s], pr, ts.dim[s]};
+    ncount[p] = ts.npts[s];
+}
+
+__global__ void k_relocate(const Task* tasks, const int32_t* task_nodes, const int32_t* task_base,
+                           const KdNode* scratch, const int32_t* scnt, KdNode* nodes, int32_t* ncount) {
+    const Task tk = tasks[blockIdx.x];
+    const int cnt = task_nodes[blockIdx.x];
+    const int base = task_base[blockIdx.x];
+    const KdNode* src = scratch + 2 * tk.start;
+    const int32_t* sc = scnt + 2 * tk.start;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        KdNode nd = src[i];
+        if (nd.db >= 0) nd.a += base;
+        nodes[base + i] = nd;
+        ncount[base + i] = sc[i];
+    }
+}
+
+__global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const int32_t* __restrict__ perm,
+                             uint64_t* __restrict__ ids_out, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) ids_out[i] = ids_in ? ids_in[perm[i]] : (uint64_t)perm[i];
+}
+
+template <typename T>
+__global__ void k_init(const T* __restrict__ in, T* __restrict__ buf, int32_t* __restrict__ idx, int64_t n, int D) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int d = 0; d < D; d++) buf[(int64_t)d * n + i] = in[(int64_t)d * n + i];
+    idx[i] = (int32_t)i;
+}
+
+__global__ void k_count_leaves(const KdNode* nodes, int64_t nn, unsigned long long* out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool leaf = i < nn && nodes[i].db < 0;
+    const unsigned b = __ballot_sync(FULL, leaf);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
+// ============================================================================
+// host orchestration
+// ============================================================================
+template <typename X>
+static X* dalloc(size_t count, cudaStream_t st) {
+    void* p = nullptr;
+    KD_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(X), st));
+    return static_cast<X*>(p);
+}
+static void dfree(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+template <typename T>
+void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const BuildCfg& cfg, cudaStream_t st,
+                KdTreeDev* out, BuildStats* stats) {
+    cudaEvent_t e0, e1;
+    KD_CUDA(cudaEventCreate(&e0));
+    KD_CUDA(cudaEventCreate(&e1));
+    KD_CUDA(cudaEventRecord(e0, st));
+    out->dims = dims;
+    out->n = n;
+    out->dtype = sizeof(T) == 4 ? DT_F32 : DT_F64;
+    KD_CUDA(cudaGetDevice(&out->device));
+    if (n == 0) {
+        out->n_nodes = 0; out->n_leaves = 0; out->depth = 0;
+        out->nodes = dalloc<KdNode>(1, st);
+        out->node_count = dalloc<int32_t>(1, st);
+        out->coords = dalloc<T>(1, st);
+        out->ids = dalloc<uint64_t>(1, st);
+        out->perm = dalloc<int32_t>(1, st);
+        KD_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    DevCtx c;
+    c.dims = dims;
+    c.N = n;
+    c.bucket = cfg.bucket;
+    c.ms = cfg.msample;
+    c.vs = cfg.vsample;
+    c.seed = cfg.seed;
+    c.ts = (int)std::min<int64_t>({(int64_t)MAXS, cfg.msample, cfg.vsample});
+    // shared-memory capacity caps the subtree size for wide / f64 points
+    int dev_smem = 0;
+    KD_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, out->device));
+    while (c.ts > 32 && SubSmem::bytes(c.ts, dims, sizeof(T)) > (size_t)dev_smem) c.ts /= 2;
+    c.ts = std::max<int>(c.ts, 1);
+
+    T* buf[2] = {dalloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
+    int32_t* idx[2] = {dalloc<int32_t>(n, st), dalloc<int32_t>(n, st)};
+    k_init<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_in, buf[0], idx[0], n, dims);
+    KD_CUDA(cudaGetLastError());
+
+    // top store (grown per level)
+    size_t ts_cap = 1024;
+    TopStore ts{};
+    auto ts_alloc = [&](size_t cap) {
+        TopStore t2{};
+        t2.dim = dalloc<int32_t>(cap, st); t2.val = dalloc<double>(cap, st);
+        t2.left = dalloc<int32_t>(cap, st); t2.right = dalloc<int32_t>(cap, st);
+        t2.npts = dalloc<int32_t>(cap, st); t2.kind = dalloc<int32_t>(cap, st);
+        t2.task = dalloc<int32_t>(cap, st); t2.nodes = dalloc<int32_t>(cap, st);
+        t2.pre = dalloc<int32_t>(cap, st);
+        return t2;
+    };
+    auto ts_free = [&](TopStore& t2) {
+        dfree(t2.dim, st); dfree(t2.val, st); dfree(t2.left, st); dfree(t2.right, st); dfree(t2.npts, st);
+        dfree(t2.kind, st); dfree(t2.task, st); dfree(t2.nodes, st); dfree(t2.pre, st);
+    };
+    ts = ts_alloc(ts_cap);
+    size_t ts_used = 1;
+    // tasks: at most one per point range; bounded by 2 * (#top nodes) + 1 -> grow with the store
+    size_t task_cap = 1024;
+    Task* tasks = dalloc<Task>(task_cap, st);
+    int* task_ctr = dalloc<int>(1, st);
+    KD_CUDA(cudaMemsetAsync(task_ctr, 0, sizeof(int), st));
+    unsigned long long* next_ctr = dalloc<unsigned long long>(1, st);
+    int* slow_count = dalloc<int>(1, st);
+    unsigned long long* h_ctr = nullptr;
+    KD_CUDA(cudaMallocHost(&h_ctr, 2 * sizeof(unsigned long long)));
+
+    std::vector<LNode*> levels;
+    std::vector<int> level_k;
+    int K = 0;
+    uint32_t tiles = 0;
+    {
+        // root
+        const int32_t kind_root = n > c.ts ? TS_INTERIOR : TS_TASK;
+        KD_CUDA(cudaMemcpyAsync(ts.kind, &kind_root, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        const int32_t zero = 0;
+        KD_CUDA(cudaMemcpyAsync(ts.pre, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        if (n > c.ts) {
+            LNode root{0, (int32_t)n, 0, 1ULL, 0, 0};
+            LNode* l0 = dalloc<LNode>(1, st);
+            KD_CUDA(cudaMemcpyAsync(l0, &root, sizeof(LNode), cudaMemcpyHostToDevice, st));
+            levels.push_back(l0);
+            K = 1;
+            tiles = (uint32_t)((n + TILE - 1) / TILE);
+        } else {
+            Task t0{0, (int32_t)n, 0, 1ULL, 0, 0, 0, 0};
+            KD_CUDA(cudaMemcpyAsync(tasks, &t0, sizeof(Task), cudaMemcpyHostToDevice, st));
+            const int one = 1;
+            KD_CUDA(cudaMemcpyAsync(task_ctr, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+            const int32_t z = 0;
+            KD_CUDA(cudaMemcpyAsync(ts.task, &z, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        }
+    }
+    size_t sample_smem = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
+    int par = 0;  // buffer holding the current level's points
+    int64_t slow_total = 0;
+    int ntasks_known = 0;
+    while (K > 0) {
+        LNode* lv = levels.back();
+        // capacity: children slots and tasks
+        if (ts_used + 2 * (size_t)K + 1 > ts_cap) {
+            size_t nc = std::max(ts_cap * 2, ts_used + 2 * (size_t)K + 1);
+            TopStore t2 = ts_alloc(nc);
+            auto cp = [&](void* d, void* s, size_t b) { KD_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, st)); };
+            cp(t2.dim, ts.dim, ts_used * 4); cp(t2.val, ts.val, ts_used * 8); cp(t2.left, ts.left, ts_used * 4);
+            cp(t2.right, ts.right, ts_used * 4); cp(t2.npts, ts.npts, ts_used * 4); cp(t2.kind, ts.kind, ts_used * 4);
+            cp(t2.task, ts.task, ts_used * 4); cp(t2.pre, ts.pre, ts_used * 4);
+            ts_free(ts);
+            ts = t2;
+            ts_cap = nc;
+        }
+        if ((size_t)ntasks_known + 2 * (size_t)K + 1 > task_cap) {
+            size_t nc = std::max(task_cap * 2, (size_t)ntasks_known + 2 * (size_t)K + 1);
+            Task* t2 = dalloc<Task>(nc, st);
+            KD_CUDA(cudaMemcpyAsync(t2, tasks, sizeof(Task) * ntasks_known, cudaMemcpyDeviceToDevice, st));
+            dfree(tasks, st);
+            tasks = t2;
+            task_cap = nc;
+        }
+        Split* split = dalloc<Split>(K, st);
+        T* wb = dalloc<T>((size_t)K * WIN, st);
+        uint32_t* wf = dalloc<uint32_t>((size_t)K * WIN, st);
+        int* slow_list = dalloc<int>(K, st);
+        uint32_t* tile_left = dalloc<uint32_t>(tiles + 1, st);
+        uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
+        KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
+        k_sample<T><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
+            buf[par], lv, K, c, split, wb, wf);
+        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, wb, wf);
+        k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
+        k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(buf[par], lv, c, split, slow_list, slow_count);
+        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, tile_left);
+        size_t tmp_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
+        void* tmp = dalloc<unsigned char>(tmp_bytes, st);
+        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
+        k_scatter<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], idx[par], buf[1 - par], idx[1 - par], lv, K, c, split,
+                                                     tile_loff);
+        LNode* next = dalloc<LNode>(2 * (size_t)K, st);
+        KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long), st));
+        k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, par, (int)ts_used, ts, next, next_ctr,
+                                                    tasks, task_ctr);
+        KD_CUDA(cudaGetLastError());
+        KD_CUDA(cudaMemcpyAsync(&h_ctr[0], next_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        KD_CUDA(cudaMemcpyAsync(&h_ctr[1], task_ctr, sizeof(int), cudaMemcpyDeviceToHost, st));
+        int* h_slow = reinterpret_cast<int*>(&h_ctr[1]) + 1;
+        KD_CUDA(cudaMemcpyAsync(h_slow, slow_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KD_CUDA(cudaStreamSynchronize(st));
+        slow_total += *h_slow;
+        ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
+        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st);
+        dfree(tile_loff, st); dfree(tmp, st);
+        level_k.push_back(K);
+        ts_used += 2 * (size_t)K;
+        K = (int)(h_ctr[0] >> 32);
+        tiles = (uint32_t)(h_ctr[0] & 0xFFFFFFFFULL);
+        par = 1 - par;
+        if (K > 0) levels.push_back(next);
+        else dfree(next, st);
+    }
+    const int ntasks = ntasks_known > 0 ? ntasks_known : 1;
+    // subtree phase
+    KdNode* scratch = dalloc<KdNode>(2 * (size_t)n + 2, st);
+    int32_t* scnt = dalloc<int32_t>(2 * (size_t)n + 2, st);
+    int32_t* task_nodes = dalloc<int32_t>(ntasks, st);
+    int32_t* task_depth = dalloc<int32_t>(ntasks, st);
+    int32_t* task_base = dalloc<int32_t>(ntasks, st);
+    const size_t sub_smem = SubSmem::bytes(c.ts, dims, sizeof(T));
+    KD_CUDA(cudaFuncSetAttribute(k_subtree<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
+    k_subtree<T><<<ntasks, SUB_THREADS, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt,
+                                                       task_nodes, task_depth);
+    KD_CUDA(cudaGetLastError());
+    // top counts bottom-up, preorder top-down
+    for (int L = (int)levels.size() - 1; L >= 0; L--)
+        k_top_count<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes);
+    int32_t total_nodes = 0;
+    {
+        int32_t root_kind = 0;
+        KD_CUDA(cudaMemcpyAsync(&root_kind, ts.kind, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        KD_CUDA(cudaStreamSynchronize(st));
+        const int32_t* src = root_kind == TS_TASK ? task_nodes : ts.nodes;
+        KD_CUDA(cudaMemcpyAsync(&total_nodes, src, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        if (root_kind == TS_TASK) KD_CUDA(cudaMemsetAsync(task_base, 0, sizeof(int32_t), st));
+        KD_CUDA(cudaStreamSynchronize(st));
+    }
+    KdNode* nodes = dalloc<KdNode>(total_nodes, st);
+    int32_t* ncount = dalloc<int32_t>(total_nodes, st);
+    for (size_t L = 0; L < levels.size(); L++)
+        k_top_pre<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes, task_base, nodes,
+                                                            ncount);
+    k_relocate<<<ntasks, 256, 0, st>>>(tasks, task_nodes, task_base, scratch, scnt, nodes, ncount);
+    uint64_t* ids_out = dalloc<uint64_t>(n, st);
+    k_gather_ids<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_ids, idx[0], ids_out, n);
+    unsigned long long* d_leaves = dalloc<unsigned long long>(1, st);
+    KD_CUDA(cudaMemsetAsync(d_leaves, 0, sizeof(unsigned long long), st));
+    k_count_leaves<<<(unsigned)((total_nodes + 255) / 256), 256, 0, st>>>(nodes, total_nodes, d_leaves);
+    KD_CUDA(cudaGetLastError());
+    // depth = max(task depths, top levels)
+    std::vector<int32_t> hdepth(ntasks);
+    KD_CUDA(cudaMemcpyAsync(hdepth.data(), task_depth, sizeof(int32_t) * ntasks, cudaMemcpyDeviceToHost, st));
+    unsigned long long hleaves = 0;
+    KD_CUDA(cudaMemcpyAsync(&hleaves, d_leaves, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    KD_CUDA(cudaEventRecord(e1, st));
+    KD_CUDA(cudaStreamSynchronize(st));
+    int64_t depth = 0;
+    for (int i = 0; i < ntasks_known; i++) depth = std::max<int64_t>(depth, hdepth[i]);
+    out->n_nodes = total_nodes;
+    out->n_leaves = (int64_t)hleaves;
+    out->depth = depth;
+    out->nodes = nodes;
+    out->node_count = ncount;
+    out->coords = buf[0];
+    out->ids = ids_out;
+    out->perm = idx[0];
+    if (stats) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        stats->ms_total = ms;
+        stats->levels = (int)levels.size();
+        stats->tasks = ntasks_known;
+        stats->slow_nodes = slow_total;
+    }
+    // release scratch
+    dfree(buf[1], st); dfree(idx[1], st);
+    for (auto l : levels) dfree(l, st);
+    ts_free(ts);
+    dfree(tasks, st); dfree(task_ctr, st); dfree(next_ctr, st); dfree(slow_count, st);
+    dfree(scratch, st); dfree(scnt, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
+    dfree(d_leaves, st);
+    cudaFreeHost(h_ctr);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    KD_CUDA(cudaStreamSynchronize(st));
+}
+
+void free_tree(KdTreeDev* t) {
+    if (!t) return;
+    cudaFree(t->nodes); cudaFree(t->node_count); cudaFree(t->coords); cudaFree(t->ids); cudaFree(t->perm);
+    t->nodes = nullptr; t->node_count = nullptr; t->coords = nullptr; t->ids = nullptr; t->perm = nullptr;
+}
+
+template void build_tree<float>(const float*, const uint64_t*, int64_t, int, const BuildCfg&, cudaStream_t, KdTreeDev*,
+                                BuildStats*);
+template void build_tree<double>(const double*, const uint64_t*, int64_t, int, const BuildCfg&, cudaStream_t,
+                                 KdTreeDev*, BuildStats*);
+
+}  // namespace kdb

@@ -1,0 +1,325 @@
+// kd_query.cu -- exact k-nearest-neighbour search (Algorithm 1, local_query.py:72-172).
+//
+// One thread per query; a warp carries 32 queries that the host orders by the
+// leaf they land in, so a warp's traversals stay coherent (same nodes, same
+// buckets -> broadcast loads from L1).  Per query:
+//   * explicit stack of far children with per-dimension box offsets;
+//   * pruning bound = sum of squared offsets evaluated in fp32 with
+//     round-toward-zero steps, which is provably <= the binary64 distance of
+//     every point in the box (monotone rounding), so pruning never loses a
+//     neighbour;
+//   * leaf scan in binary64 with the reference's exact operation order
+//     (core.py:199-228: ascending dimension, no FMA) -> bit-identical keys;
+//   * top-k kept sorted by (sq_dist, point_id) in registers (k <= 32) or as the
+//     reference's bounded max-heap in global scratch (any k);
+//   * tie semantics of the brute-force oracle (pkg/tests/conftest.py:8-18):
+//     admit d < radius while under-full, replace on lexicographic (d, id) when
+//     full, prune only when bound > k-th distance.  (The reference prunes at
+//     bound >= r' and can lose an exact tie with a smaller id: SURVEY §8(a) Q5.)
+#include <cub/cub.cuh>
+
+#include "kd_common.cuh"
+#include "kd_query.cuh"
+#include "kd_tree.cuh"
+
+namespace kdb {
+
+constexpr int QCAP = 64;  // traversal stack capacity (tree depth + 2)
+
+__device__ __forceinline__ bool lexless(double d0, uint64_t i0, double d1, uint64_t i1) {
+    return d0 < d1 || (d0 == d1 && i0 < i1);
+}
+
+template <int DT>
+struct Dims {
+    static constexpr int cap = DT > 0 ? DT : 16;
+};
+
+template <typename T, int DT, int KM>
+__global__ void __launch_bounds__(128)
+k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
+      const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
+      const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
+      const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
+      int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, double* __restrict__ heap_d,
+      uint64_t* __restrict__ heap_i) {
+    constexpr int DC = Dims<DT>::cap;
+    const int D = DT > 0 ? DT : dims_rt;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nq) return;
+    const int64_t qi = order ? (int64_t)order[t] : t;
+    double q[DC];
+#pragma unroll
+    for (int d = 0; d < DC; d++) q[d] = d < D ? queries[qi * D + d] : 0.0;
+    const double radius = radii ? radii[qi] : INFINITY;
+    const uint64_t ex = excl ? excl[qi] : ~0ULL;
+    const bool has_ex = excl != nullptr;
+    int64_t c0 = 0, c1 = 0, c2 = 0;
+
+    // top-k state
+    double bd[KM > 0 ? KM : 1];
+    uint64_t bi[KM > 0 ? KM : 1];
+    double* hd = nullptr;
+    uint64_t* hi = nullptr;
+    if (KM == 0) {
+        hd = heap_d + qi * (int64_t)k;
+        hi = heap_i + qi * (int64_t)k;
+    }
+    int cnt = 0;
+    double kth_d = radius;       // pruning radius: radius while under-full, k-th distance when full
+    uint64_t kth_i = 0;
+
+    // traversal stack
+    int st_node[QCAP];
+    float st_off[QCAP][DC];
+    int sp = 0;
+    float off[DC];
+#pragma unroll
+    for (int d = 0; d < DC; d++) off[d] = 0.0f;
+
+    auto admissible = [&](float b) {
+        const double bb = (double)b;
+        return cnt < k ? bb < radius : bb <= kth_d;
+    };
+
+    int node = n_nodes > 0 ? 0 : -1;
+    while (node >= 0) {
+        c0++;
+        const KdNode rec = nodes[node];
+        if (rec.db >= 0) {
+            const int dim = rec.db;
+            double qd = q[0];
+#pragma unroll
+            for (int d = 1; d < DC; d++)
+                if (d == dim) qd = q[d];
+            const double diff = qd - rec.v;  // q - v
+            const bool goleft = qd < rec.v;
+            const int near = goleft ? node + 1 : rec.a;
+            const int far = goleft ? rec.a : node + 1;
+            // far box: offset along dim becomes |q - v| (rounded toward zero)
+            float fo[DC];
+#pragma unroll
+            for (int d = 0; d < DC; d++) fo[d] = off[d];
+            float ad = __double2float_rz(fabs(diff));
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d == dim) fo[d] = ad;
+            float fb = 0.0f;
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
+            if (admissible(fb) && sp < QCAP) {
+                st_node[sp] = far;
+#pragma unroll
+                for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
+                sp++;
+            }
+            node = near;
+            continue;
+        }
+        // leaf bucket scan
+        const int start = rec.a, len = -1 - rec.db;
+        c1++;
+        c2 += len;
+        for (int i = start; i < start + len; i++) {
+            double dist = 0.0;
+#pragma unroll
+            for (int d = 0; d < DC; d++) {
+                if (d < D) {
+                    const double df = __dsub_rn((double)coords[(int64_t)d * n + i], q[d]);
+                    dist = __dadd_rn(dist, __dmul_rn(df, df));
+                }
+            }
+            if (cnt < k) {
+                if (!(dist < radius)) continue;
+            } else if (!(dist <= kth_d)) {
+                continue;
+            }
+            const uint64_t id = ids[i];
+            if (has_ex && id == ex) continue;
+            if (KM > 0) {
+                if (cnt == k && !lexless(dist, id, kth_d, kth_i)) continue;
+                const int p = cnt < k ? cnt : k - 1;
+#pragma unroll
+                for (int j = 0; j < (KM > 0 ? KM : 1); j++)
+                    if (j == p) { bd[j] = dist; bi[j] = id; }
+#pragma unroll
+                for (int j = (KM > 0 ? KM : 1) - 1; j >= 1; j--) {
+                    if (j <= p && lexless(bd[j], bi[j], bd[j - 1], bi[j - 1])) {
+                        const double td = bd[j]; bd[j] = bd[j - 1]; bd[j - 1] = td;
+                        const uint64_t ti = bi[j]; bi[j] = bi[j - 1]; bi[j - 1] = ti;
+                    }
+                }
+                if (cnt < k) cnt++;
+                if (cnt == k) {
+#pragma unroll
+                    for (int j = 0; j < (KM > 0 ? KM : 1); j++)
+                        if (j == k - 1) { kth_d = bd[j]; kth_i = bi[j]; }
+                }
+            } else {
+                // the reference's bounded max-heap (local_query.py:36-69)
+                if (cnt < k) {
+                    int ii = cnt;
+                    hd[ii] = dist; hi[ii] = id;
+                    while (ii > 0) {
+                        const int pp = (ii - 1) / 2;
+                        if (lexless(hd[pp], hi[pp], hd[ii], hi[ii])) {
+                            double td = hd[pp]; hd[pp] = hd[ii]; hd[ii] = td;
+                            uint64_t ti = hi[pp]; hi[pp] = hi[ii]; hi[ii] = ti;
+                            ii = pp;
+                        } else break;
+                    }
+                    cnt++;
+                } else {
+                    if (!lexless(dist, id, hd[0], hi[0])) continue;
+                    hd[0] = dist; hi[0] = id;
+                    int ii = 0;
+                    for (;;) {
+                        const int l = 2 * ii + 1, r = l + 1;
+                        int big = ii;
+                        if (l < cnt && lexless(hd[big], hi[big], hd[l], hi[l])) big = l;
+                        if (r < cnt && lexless(hd[big], hi[big], hd[r], hi[r])) big = r;
+                        if (big == ii) break;
+                        double td = hd[big]; hd[big] = hd[ii]; hd[ii] = td;
+                        uint64_t ti = hi[big]; hi[big] = hi[ii]; hi[ii] = ti;
+                        ii = big;
+                    }
+                }
+                if (cnt == k) { kth_d = hd[0]; kth_i = hi[0]; }
+            }
+        }
+        // pop the next admissible far child
+        node = -1;
+        while (sp > 0) {
+            sp--;
+            float po[DC];
+#pragma unroll
+            for (int d = 0; d < DC; d++) po[d] = st_off[sp][d];
+            float pb = 0.0f;
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d < D) pb = __fadd_rz(pb, __fmul_rz(po[d], po[d]));
+            if (admissible(pb)) {
+                node = st_node[sp];
+#pragma unroll
+                for (int d = 0; d < DC; d++) off[d] = po[d];
+                break;
+            }
+            c0++;  // popped and pruned (counted like the reference's visit of a pruned node)
+        }
+    }
+    // results: ascending (sq_dist, id)
+    out_c[qi] = cnt;
+    if (KM > 0) {
+#pragma unroll
+        for (int j = 0; j < (KM > 0 ? KM : 1); j++) {
+            if (j < cnt) {
+                out_d[qi * (int64_t)k + j] = bd[j];
+                out_i[qi * (int64_t)k + j] = bi[j];
+            }
+        }
+    } else {
+        int hs = cnt, j = cnt;
+        while (hs > 0) {
+            j--;
+            out_d[qi * (int64_t)k + j] = hd[0];
+            out_i[qi * (int64_t)k + j] = hi[0];
+            hs--;
+            if (hs > 0) {
+                hd[0] = hd[hs]; hi[0] = hi[hs];
+                int ii = 0;
+                for (;;) {
+                    const int l = 2 * ii + 1, r = l + 1;
+                    int big = ii;
+                    if (l < hs && lexless(hd[big], hi[big], hd[l], hi[l])) big = l;
+                    if (r < hs && lexless(hd[big], hi[big], hd[r], hi[r])) big = r;
+                    if (big == ii) break;
+                    double td = hd[big]; hd[big] = hd[ii]; hd[ii] = td;
+                    uint64_t ti = hi[big]; hi[big] = hi[ii]; hi[ii] = ti;
+                    ii = big;
+                }
+            }
+        }
+    }
+    if (out_ctr) {
+        out_ctr[qi * 3 + 0] = c0;
+        out_ctr[qi * 3 + 1] = c1;
+        out_ctr[qi * 3 + 2] = c2;
+    }
+}
+
+// leaf reached by descending with the tie rule (coord >= value goes right);
+// used as the sort key that makes each warp's 32 queries spatially coherent
+template <int DT>
+__global__ void k_leaf_of(const KdNode* __restrict__ nodes, int64_t n_nodes, const double* __restrict__ queries,
+                          int dims_rt, int64_t nq, uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+    const int D = DT > 0 ? DT : dims_rt;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    int node = 0;
+    if (n_nodes > 0) {
+        for (;;) {
+            const KdNode rec = nodes[node];
+            if (rec.db < 0) break;
+            node = queries[i * D + rec.db] < rec.v ? node + 1 : rec.a;
+        }
+    }
+    key[i] = (uint32_t)node;
+    val[i] = (int32_t)i;
+}
+
+template <typename T, int DT, int KM>
+static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st) {
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((a.nq + threads - 1) / threads);
+    k_knn<T, DT, KM><<<blocks, threads, 0, st>>>(t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n,
+                                                 t.dims, a.queries, order, a.nq, (int)a.k, a.radii, a.excl, a.out_d,
+                                                 a.out_i, a.out_c, a.out_ctr, a.heap_d, a.heap_i);
+}
+
+template <typename T, int DT>
+static void dispatch_k(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st) {
+    if (a.k <= 8) launch_knn<T, DT, 8>(t, a, order, st);
+    else if (a.k <= 16) launch_knn<T, DT, 16>(t, a, order, st);
+    else if (a.k <= 32) launch_knn<T, DT, 32>(t, a, order, st);
+    else launch_knn<T, DT, 0>(t, a, order, st);
+}
+
+template <typename T>
+static void dispatch_d(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st) {
+    if (t.dims == 2) dispatch_k<T, 2>(t, a, order, st);
+    else if (t.dims == 3) dispatch_k<T, 3>(t, a, order, st);
+    else dispatch_k<T, 0>(t, a, order, st);
+}
+
+void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return;
+    int32_t* order = nullptr;
+    void* tmp = nullptr;
+    uint32_t *k0 = nullptr, *k1 = nullptr;
+    int32_t* v0 = nullptr;
+    if (a.sort_queries && a.nq > 1 && t.n_nodes > 1) {
+        KD_CUDA(cudaMallocAsync((void**)&k0, a.nq * 4, st));
+        KD_CUDA(cudaMallocAsync((void**)&k1, a.nq * 4, st));
+        KD_CUDA(cudaMallocAsync((void**)&v0, a.nq * 4, st));
+        KD_CUDA(cudaMallocAsync((void**)&order, a.nq * 4, st));
+        const unsigned blocks = (unsigned)((a.nq + 255) / 256);
+        if (t.dims == 3) k_leaf_of<3><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
+        else k_leaf_of<0><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
+        int bits = 1;
+        while (bits < 32 && ((int64_t)1 << bits) < t.n_nodes) bits++;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
+        KD_CUDA(cudaMallocAsync(&tmp, tb, st));
+        cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
+    }
+    if (t.dtype == DT_F32) dispatch_d<float>(t, a, order, st);
+    else dispatch_d<double>(t, a, order, st);
+    KD_CUDA(cudaGetLastError());
+    if (order) {
+        cudaFreeAsync(k0, st); cudaFreeAsync(k1, st); cudaFreeAsync(v0, st); cudaFreeAsync(order, st);
+        cudaFreeAsync(tmp, st);
+    }
+}
+
+}  // namespace kdb

@@ -1,0 +1,29 @@
+// kd_query.cuh -- exact KNN entry point (device pointers only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kd_tree.cuh"
+
+namespace kdb {
+
+struct KnnArgs {
+    const double* queries = nullptr;  // [nq][dims] row-major binary64
+    int64_t nq = 0;
+    int64_t k = 1;
+    const double* radii = nullptr;    // [nq] squared radii (nullptr = +inf)
+    const uint64_t* excl = nullptr;   // [nq] id to exclude per query (nullptr = none)
+    double* out_d = nullptr;          // [nq][k]
+    uint64_t* out_i = nullptr;        // [nq][k]
+    int64_t* out_c = nullptr;         // [nq]
+    int64_t* out_ctr = nullptr;       // [nq][3] or nullptr
+    double* heap_d = nullptr;         // [nq][k] scratch when k > 32
+    uint64_t* heap_i = nullptr;
+    bool sort_queries = true;
+};
+
+constexpr int KNN_MAX_DEPTH = 61;  // traversal stack capacity - 3
+
+void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st);
+
+}  // namespace kdb
