@@ -1257,11 +1257,13 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
             KD_CUDA(cudaMemcpyAsync(ts.task, &z, sizeof(int32_t), cudaMemcpyHostToDevice, st));
         }
     }
+    int ntasks_known = K == 0 ? 1 : 0;
+    {
+    }
     size_t sample_smem = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
     KD_CUDA(cudaFuncSetAttribute(k_sample<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
-    int ntasks_known = 0;
     while (K > 0) {
         LNode* lv = levels.back();
         // capacity: children slots and tasks
