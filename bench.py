@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: kd-tree build (Mpoints/s) + exact KNN (queries/s) on B200.
+
+Workload (BASELINE.json configs[1], SURVEY §8(d) "C2"): 64,000,000 clustered 3D
+float32 points (4096 Gaussian halos + 20 % uniform background, periodic box),
+16,000,000 queries drawn from the dataset rows with the self-match excluded,
+k=5, leaf bucket 32.  One step = build the whole kd-tree + answer every query.
+
+Printed JSON (one line, rank 0):
+  value        build throughput, device-resident inputs (Mpoints/s)
+  knn          query throughput for the same step (queries/s) + its roofline
+  roofline     build: algorithmic bytes N*L*(8D+12) per build / build time vs
+               the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  e2e          the same two metrics through the C-ABI with pinned HOST buffers,
+               host<->device copies inside the timed region
+  cpu_baseline the reference algorithm (C oracle port, all host cores) on a
+               bounded sample; its traversal over the (identical) full-size
+               tree also yields the reference counters used by the query model
+  --impl reference  times that CPU port as the reference arm
+
+Multi-GPU (torchrun, N>1): weak scaling -- each rank owns its own 64M points
+and 16M queries; see DESIGN.md §6 for the distributed engine.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--n", type=int, default=None, help="override point count (debug)")
+    p.add_argument("--q", type=int, default=None, help="override query count (debug)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-build-sample", type=int, default=4_000_000)
+    p.add_argument("--cpu-query-sample", type=int, default=200_000)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        sm_load = sorted(sm)
+        med = sm_load[len(sm_load) // 2] if sm_load else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "samples": len(sm), "power_w_max": max(power) if power else None,
+                "reasons": sorted(reasons)}
+
+
+def build_bytes(n, dims, leaf):
+    """B_build = N * L * (8D + 12), L = ceil(log2(N / leaf))."""
+    levels = max(1, math.ceil(math.log2(max(n / leaf, 2))))
+    return n * levels * (8 * dims + 12), levels
+
+
+def query_bytes(dims, k, v, c):
+    """B_q = 4D + 8V + 4D*C + 16k (V, C: reference counters)."""
+    return 4 * dims + 8 * v + 4 * dims * c + 16 * k
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_baseline_leg(cfgname, w, tree, sel_queries, args, seed=0):
+    """The reference algorithm (C oracle port of kdknn build_local_tree /
+    find_knn_batch) on the host cores: build of a bounded sample of the same
+    law, and the reference traversal over the full-size tree (identical bytes to
+    the GPU tree) for a query sample -> CPU rates + reference counters."""
+    import numpy as np
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    nb = min(args.cpu_build_sample, w.n)
+    rows = __import__("paper_1607_08220_b200.workloads", fromlist=["x"]).make_points_numpy(cfgname, nb, seed=77)
+    coords = np.ascontiguousarray(rows.T.astype(np.float64))
+    O.build_tree(coords[:, :100_000], bucket_size=w.leaf, seed=seed, threads=cores)  # warm
+    t0 = time.perf_counter()
+    O.build_tree(coords, bucket_size=w.leaf, seed=seed, threads=cores)
+    tb = time.perf_counter() - t0
+    # reference traversal over the full tree for a query sample
+    otree = O.OracleTree(tree.node_dim, tree.node_value, tree.node_left, tree.node_right, tree.node_count,
+                         None, tree.points.coords, tree.points.ids, tree.depth)
+    qs = sel_queries
+    kk = w.k + (1 if w.queries_from_data else 0)
+    t0 = time.perf_counter()
+    _, _, _, ctr = O.knn(otree, qs, kk, threads=cores)
+    tq = time.perf_counter() - t0
+    return {
+        "build_mpts_s": nb / tb / 1e6, "build_sample_points": nb, "build_s": tb,
+        "knn_q_s": qs.shape[0] / tq, "knn_sample_queries": int(qs.shape[0]), "knn_s": tq,
+        "ref_nodes_visited": float(ctr[:, 0].mean()), "ref_points_compared": float(ctr[:, 2].mean()),
+        "cores": cores,
+    }
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (C oracle port) on host cores."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1607_08220_b200.workloads import CONFIGS, make_points_numpy
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    nb = min(args.cpu_build_sample, w.n)
+    nqs = min(args.cpu_query_sample, w.q)
+    rows = make_points_numpy(args.config, nb, seed=77)
+    coords = np.ascontiguousarray(rows.T.astype(np.float64))
+    rng = np.random.default_rng(5)
+    sel = rng.choice(nb, size=min(nqs, nb), replace=False)
+    queries = rows[sel].astype(np.float64)
+    kk = w.k + (1 if w.queries_from_data else 0)
+    tb_all, tq_all = [], []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        tree = O.build_tree(coords, bucket_size=w.leaf, seed=0, threads=cores)
+        t1 = time.perf_counter()
+        O.knn(tree, queries, kk, threads=cores)
+        t2 = time.perf_counter()
+        if step >= args.warmup:
+            tb_all.append(t1 - t0)
+            tq_all.append(t2 - t1)
+    tb, tq = float(np.mean(tb_all)), float(np.mean(tq_all))
+    value = nb / tb / 1e6
+    line = {
+        "impl": "reference", "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5)", "value": value,
+        "unit": "Mpoints/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "q": w.q, "k": w.k, "leaf": w.leaf, "dims": w.dims},
+        "knn": {"value": len(sel) / tq, "unit": "queries/s"},
+        "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": cores, "kind": "port",
+                         "sample": f"build of {nb} points of the {w.name} law + {len(sel)} self-excluded "
+                                   f"queries (k+1) against that tree, per step; C restatement of the reference "
+                                   f"(oracle/kdknn_oracle.c), OpenMP {cores} threads"},
+        "e2e": {"value": value, "unit": "Mpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------------------------
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1607_08220_b200 import _native as N
+    from paper_1607_08220_b200.local_query import find_knn_device
+    from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
+    from paper_1607_08220_b200.workloads import CONFIGS, make_points, make_queries
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    w = CONFIGS[args.config]
+    n = args.n or w.n
+    q = args.q or w.q
+    rows = make_points(args.config, dev, seed=1000 + rank, n=n)
+    coords = rows.t().contiguous()
+    queries, excl = make_queries(args.config, rows, dev, seed=2000 + rank, q=q)
+    cfg = BuildConfig(bucket_size=w.leaf, seed=0)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+
+    def step(record=None):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        tree = build_local_tree_device(coords, None, cfg)
+        e1.record(stream)
+        out = find_knn_device(tree, queries, w.k, exclude_ids=excl)
+        e2.record(stream)
+        return tree, out, (e0, e1, e2)
+
+    for _ in range(args.warmup):
+        tree, out, _ = step()
+        del tree, out
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    evs = []
+    levels = 0
+    tree = None
+    for _ in range(args.steps):
+        del tree
+        tree, out, ev = step()
+        evs.append(ev)
+        levels = tree.build_info["levels"]
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    tb = sum(a.elapsed_time(b) for a, b, _ in evs) / len(evs) / 1e3
+    tq = sum(b.elapsed_time(c) for _, b, c in evs) / len(evs) / 1e3
+    if world > 1:
+        t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, tq = t.tolist()
+
+    # --- sanity: a sample of this step's results vs an exact fp64 brute force on device
+    od, oi, oc, _ = out
+    ok = True
+    cols = [rows[:, d].to(torch.float64) for d in range(w.dims)]
+    for j in range(min(16, q)):
+        dd = (cols[0] - queries[j, 0]) ** 2
+        for d in range(1, w.dims):
+            dd += (cols[d] - queries[j, d]) ** 2
+        if excl is not None:
+            dd[excl[j]] = float("inf")
+        kth = torch.topk(dd, w.k, largest=False).values.max()
+        cand = torch.nonzero(dd <= kth).flatten()  # ascending ids
+        order = torch.sort(dd[cand], stable=True).indices[:w.k]
+        ok &= bool(torch.equal(od[j], dd[cand][order]) and torch.equal(oi[j], cand[order]))
+    del cols
+
+    # --- e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_coords = coords.cpu().pin_memory()
+        h_q = queries.cpu().pin_memory()
+        h_ex = excl.cpu().pin_memory() if excl is not None else None
+        h_d = torch.empty((q, w.k), dtype=torch.float64).pin_memory()
+        h_i = torch.empty((q, w.k), dtype=torch.int64).pin_memory()
+        h_c = torch.empty((q,), dtype=torch.int64).pin_memory()
+        cfgn = cfg.native()
+        st = C.c_void_p(stream.cuda_stream)
+        tbe, tqe = [], []
+        for it in range(2 + min(args.steps, 3)):
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            c = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h = C.c_void_p()
+            N.check(N.lib.kd_tree_build(h_coords.data_ptr(), N.KD_F32, n, w.dims, None, C.byref(cfgn), local, 0,
+                                        st, C.byref(h)))
+            b.record(stream)
+            N.check(N.lib.kd_knn(h, h_q.data_ptr(), q, w.k, None,
+                                 h_ex.data_ptr() if h_ex is not None else None, h_d.data_ptr(), h_i.data_ptr(),
+                                 h_c.data_ptr(), None, 0, st))
+            c.record(stream)
+            torch.cuda.synchronize()
+            N.lib.kd_tree_free(h)
+            if it >= 2:
+                tbe.append(a.elapsed_time(b) / 1e3)
+                tqe.append(b.elapsed_time(c) / 1e3)
+        tbe_m, tqe_m = float(np.mean(tbe)), float(np.mean(tqe))
+        if world > 1:
+            t = torch.tensor([tbe_m, tqe_m], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tbe_m, tqe_m = t.tolist()
+        e2e = {"value": world * n / tbe_m / 1e6, "unit": "Mpoints/s",
+               "knn": {"value": world * q / tqe_m, "unit": "queries/s"},
+               "h2d_bytes_per_step": int(n * w.dims * 4 + q * w.dims * 8 + (q * 8 if excl is not None else 0)),
+               "d2h_bytes_per_step": int(q * w.k * 16 + q * 8),
+               "ms_build": tbe_m * 1e3, "ms_knn": tqe_m * 1e3,
+               "path": "kd_tree_build + kd_knn (C-ABI) with pinned host buffers"}
+        del h_coords, h_q, h_ex, h_d, h_i, h_c
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        nqs = min(args.cpu_query_sample, q)
+        qsel = queries[:nqs].cpu().numpy()
+        cpu = cpu_baseline_leg(args.config, w, tree, qsel, args)
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        bbytes, levels_model = build_bytes(n, w.dims, w.leaf)
+        ach_b = bbytes / tb / 1e9
+        if cpu is not None:
+            v_ref, c_ref = cpu["ref_nodes_visited"], cpu["ref_points_compared"]
+            ctr_src = "reference counters (oracle traversal over the identical full-size tree, sample)"
+        else:
+            v_ref, c_ref, ctr_src = 44.8, 156.3, "SURVEY §8(d) C2-like counters at 4M points"
+        qb = query_bytes(w.dims, w.k, v_ref, c_ref)
+        ach_q = q * qb / tq / 1e9
+        launches = levels * 9 + 5 + 2
+        line = {
+            "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
+            "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": n, "q": q, "k": w.k, "leaf": w.leaf, "dims": w.dims,
+                       "coords": "float32 SoA (binary64 arithmetic)",
+                       "l2": "inputs larger than L2 (points %.0f MB, queries %.0f MB)" % (n * w.dims * 4 / 1e6,
+                                                                                      q * w.dims * 8 / 1e6),
+                       "parallelism": f"weak x{world}"},
+            "ms_build": tb * 1e3, "ms_knn": tq * 1e3,
+            "roofline": {"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s", "frac": ach_b / peak,
+                         "traffic": None, "kernel": "whole build (all build kernels of one kd_tree_build)",
+                         "algorithmic_bytes": bbytes, "model": f"N*L*(8D+12), L={levels_model}",
+                         "peak_kind": peak_kind},
+            "knn": {"value": world * q / tq, "unit": "queries/s",
+                    "roofline": {"bound": "hbm", "achieved": ach_q, "peak": peak, "unit": "GB/s",
+                                 "frac": ach_q / peak, "traffic": None, "kernel": "k_knn",
+                                 "bytes_per_query": qb, "model": "4D+8V+4DC+16k", "V": v_ref, "C": c_ref,
+                                 "counters": ctr_src}},
+            "sample_check_vs_fp64_bruteforce": ok,
+            "build_levels": levels,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": None if cpu is None else {
+                "value": cpu["build_mpts_s"], "unit": "Mpoints/s", "cores": cpu["cores"], "kind": "port",
+                "knn_value": cpu["knn_q_s"], "knn_unit": "queries/s",
+                "sample": f"build of {cpu['build_sample_points']} points of the same law; reference traversal of "
+                          f"{cpu['knn_sample_queries']} queries over the full-size tree (k+1 for self-exclusion)"},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

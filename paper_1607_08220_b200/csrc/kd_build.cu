@@ -1163,6 +1163,20 @@ static void dfree(void* p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
 }
 
+// keep freed stream-ordered allocations in the pool across the per-level host
+// synchronisations (the default release threshold of 0 returns them to the
+// driver at every sync and re-maps them on the next level)
+void retain_pool(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
 template <typename T>
 void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const BuildCfg& cfg, cudaStream_t st,
                 KdTreeDev* out, BuildStats* stats) {
@@ -1174,6 +1188,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     out->n = n;
     out->dtype = sizeof(T) == 4 ? DT_F32 : DT_F64;
     KD_CUDA(cudaGetDevice(&out->device));
+    retain_pool(out->device);
     if (n == 0) {
         out->n_nodes = 0; out->n_leaves = 0; out->depth = 0;
         out->nodes = dalloc<KdNode>(1, st);

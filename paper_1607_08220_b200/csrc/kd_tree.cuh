@@ -53,5 +53,6 @@ void build_tree(const T* d_coords_soa, const uint64_t* d_ids, int64_t n, int dim
                 cudaStream_t st, KdTreeDev* out, BuildStats* stats);
 
 void free_tree(KdTreeDev* t);
+void retain_pool(int device);
 
 }  // namespace kdb
