@@ -24,6 +24,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "kd_common.cuh"
@@ -37,8 +39,6 @@ constexpr int WIN = 256;         // histogram window (boundaries)
 constexpr int TILE = 4096;       // elements per tile CTA
 constexpr int TILE_THREADS = 256;
 constexpr int SAMPLE_WARPS = 4;
-constexpr int SUB_THREADS = 256;
-constexpr int SUB_WARPS = SUB_THREADS / 32;
 constexpr int SLOW_THREADS = 256;
 constexpr double U64 = 1.1102230246251565e-16;  // 2^-53
 
@@ -255,6 +255,7 @@ template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
        const T* __restrict__ wb, uint32_t* __restrict__ wf) {
+    constexpr int EPT = TILE / TILE_THREADS;
     __shared__ T sb[WIN];
     __shared__ uint32_t sf[WIN];
     __shared__ unsigned long long sL;
@@ -263,26 +264,35 @@ k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     const int nw = sp.whi - sp.wlo;
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
+    const T* row = src + (int64_t)sp.dim * c.N + nd.start;
+    // issue every load of the tile before touching shared memory
+    T v[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; j++) {
+        const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
+        v[j] = e < e1 ? row[e] : T(0);
+    }
     for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
         sf[i] = 0;
         if (i < nw) sb[i] = wb[(int64_t)ni * WIN + i];
     }
     if (threadIdx.x == 0) sL = 0;
     __syncthreads();
-    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
-    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
-    const T* row = src + (int64_t)sp.dim * c.N + nd.start;
     const T lo_b = sb[0], hi_b = sb[nw - 1];
     unsigned long long lc = 0;
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        const T v = row[e];
-        if (v < lo_b) {
+#pragma unroll
+    for (int j = 0; j < EPT; j++) {
+        const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
+        if (e >= e1) continue;
+        if (v[j] < lo_b) {
             lc++;
-        } else if (v < hi_b) {
+        } else if (v[j] < hi_b) {
             int lo = 1, hi = nw - 1;  // upper_bound over the window
             while (lo < hi) {
                 const int md = (lo + hi) >> 1;
-                if (sb[md] <= v) lo = md + 1; else hi = md;
+                if (sb[md] <= v[j]) lo = md + 1; else hi = md;
             }
             atomicAdd(&sf[lo], 1u);
         }
@@ -577,6 +587,7 @@ template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c,
         const Split* __restrict__ split, uint32_t* tile_left) {
+    constexpr int EPT = TILE / TILE_THREADS;
     __shared__ uint32_t red[TILE_THREADS / 32];
     const uint32_t t = blockIdx.x;
     const int ni = tile_node(nodes, K, t);
@@ -587,7 +598,17 @@ k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCt
         const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
         const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
         const T* row = src + (int64_t)sp.dim * c.N + nd.start;
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) cnt += (double)row[e] < sp.value;
+        T v[EPT];
+#pragma unroll
+        for (int j = 0; j < EPT; j++) {
+            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
+            v[j] = e < e1 ? row[e] : T(0);
+        }
+#pragma unroll
+        for (int j = 0; j < EPT; j++) {
+            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
+            cnt += (e < e1) && ((double)v[j] < sp.value);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
@@ -599,54 +620,98 @@ k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCt
     }
 }
 
-template <typename T>
+// stable scatter of one tile: CH chunks of 256 elements per pass; every load of
+// a pass is issued before the single block-wide prefix over (chunk, warp) counts
+template <typename T, int DT, int CH>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
           int32_t* __restrict__ idst, const LNode* __restrict__ nodes, int K, DevCtx c,
           const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff) {
-    __shared__ uint32_t wl[TILE_THREADS / 32];
+    constexpr int NW = TILE_THREADS / 32;
+    constexpr int DC = DT > 0 ? DT : 16;
+    __shared__ uint32_t wl[CH * NW];
+    __shared__ uint32_t wpre[CH * NW];
     const uint32_t t = blockIdx.x;
     const int ni = tile_node(nodes, K, t);
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     if (sp.status != ST_SPLIT) return;
+    const int D = DT > 0 ? DT : c.dims;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
     const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
     const uint32_t lbefore = tile_loff[t] - tile_loff[nd.tile_off];  // lefts in earlier tiles of this node
     int64_t lrun = lbefore;
     int64_t rrun = e0 - lbefore;
-    const int D = c.dims;
     const int64_t N = c.N;
-    const T* srow = src + (int64_t)sp.dim * N + nd.start;
-    for (int64_t base = e0; base < e1; base += TILE_THREADS) {
-        const int64_t e = base + threadIdx.x;
-        const bool valid = e < e1;
-        const bool f = valid && (double)srow[e] < sp.value;
-        const unsigned bal = __ballot_sync(FULL, f);
-        const unsigned vbal = __ballot_sync(FULL, valid);
-        if (lane == 0) wl[warp] = __popc(bal);
+    const int64_t gbase = nd.start;
+    for (int64_t pass = e0; pass < e1; pass += (int64_t)CH * TILE_THREADS) {
+        T x[CH][DC];
+        int32_t id[CH];
+        bool f[CH];
+        unsigned bal[CH];
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            const int64_t e = pass + j * TILE_THREADS + threadIdx.x;
+            const bool valid = e < e1;
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d < D) x[j][d] = valid ? src[(int64_t)d * N + gbase + e] : T(0);
+            id[j] = valid ? isrc[gbase + e] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            const int64_t e = pass + j * TILE_THREADS + threadIdx.x;
+            T xv = x[j][0];
+#pragma unroll
+            for (int d = 1; d < DC; d++)
+                if (d == sp.dim) xv = x[j][d];
+            f[j] = e < e1 && (double)xv < sp.value;
+            bal[j] = __ballot_sync(FULL, f[j]);
+            if (lane == 0) wl[j * NW + warp] = __popc(bal[j]);
+        }
         __syncthreads();
-        uint32_t lw = 0, ltot = 0, vw = 0;
-        for (int w = 0; w < TILE_THREADS / 32; w++) {
-            const uint32_t x = wl[w];
-            if (w < warp) lw += x;
-            ltot += x;
+        if (warp == 0) {  // exclusive prefix over (chunk, warp) in element order
+            constexpr int PER = (CH * NW + 31) / 32;
+            uint32_t loc[PER], s = 0;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int i = lane * PER + q;
+                loc[q] = s;
+                s += i < CH * NW ? wl[i] : 0;
+            }
+            uint32_t incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t ex = incl - s;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int i = lane * PER + q;
+                if (i < CH * NW) wpre[i] = ex + loc[q];
+            }
+            if (lane == 31) wl[0] = incl;  // pass total (wl no longer needed)
         }
-        (void)vw;
-        const uint32_t lp = lw + __popc(bal & ((1u << lane) - 1));
-        const int64_t chunk_valid = min((int64_t)TILE_THREADS, e1 - base);
-        if (valid) {
-            int64_t pos;
-            if (f) pos = lrun + lp;
-            else pos = sp.nl + rrun + (threadIdx.x - lp);
-            const int64_t gs = nd.start + e, gd = nd.start + pos;
-            for (int d = 0; d < D; d++) dst[(int64_t)d * N + gd] = src[(int64_t)d * N + gs];
-            idst[gd] = isrc[gs];
+        __syncthreads();
+        const uint32_t ltot = wl[0];
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            const int64_t e = pass + j * TILE_THREADS + threadIdx.x;
+            if (e >= e1) continue;
+            const uint32_t lp = wpre[j * NW + warp] + __popc(bal[j] & ((1u << lane) - 1));
+            const int64_t before = e - pass;  // elements of this pass before e
+            const int64_t pos = f[j] ? lrun + lp : sp.nl + rrun + (before - lp);
+            const int64_t gd = gbase + pos;
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d < D) dst[(int64_t)d * N + gd] = x[j][d];
+            idst[gd] = id[j];
         }
-        (void)vbal;
+        const int64_t pass_n = min((int64_t)CH * TILE_THREADS, e1 - pass);
         lrun += ltot;
-        rrun += chunk_valid - ltot;
+        rrun += pass_n - ltot;
         __syncthreads();
     }
 }
@@ -710,44 +775,118 @@ __global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* 
 }
 
 // ============================================================================
-// k_subtree: one CTA builds a whole subtree of <= ts points in shared memory
+// k_subtree: one warp builds a whole subtree of <= ts points, depth first in
+// preorder (local_tree.py:236-317 _build_subtree), points staged in shared
+// memory.  For n <= min(local_sample_m, variance_sample) the reference's
+// samples are the whole node, so split selection reduces to: the max-variance
+// non-constant dimension (certified binary64 sums, exact sequential fallback),
+// then the two distinct values around rank n/2 (radix select) compared with
+// the binary64 rule of median.py:143-166.
 // ============================================================================
-struct SubSmem {
-    // sizes (elements) for a given ts, dims, T
-    static __host__ __device__ size_t bytes(int ts, int dims, int tsize) {
-        size_t b = 0;
-        b += (size_t)dims * ts * tsize;  // coords
-        b = (b + 15) & ~size_t(15);
-        b += (size_t)ts * 4;             // orig ids
-        b += (size_t)2 * ts * 2;         // perm ping-pong
-        b = (b + 15) & ~size_t(15);
-        const int ns = 2 * ts + 2;
-        b += (size_t)ns * 8;             // split values (double)
-        b += (size_t)ns * 2 * 5;         // start, cnt, left, right, cnt/pre scratch
-        b += (size_t)ns * 2;             // pre
-        b += (size_t)ns;                 // dim (int8)
-        b = (b + 15) & ~size_t(15);
-        const int nl = ts / 2 + 2;
-        b += (size_t)2 * nl * 8;         // level list paths
-        b += (size_t)2 * nl * 2;         // level list slots
-        b += (size_t)(ts + 2) * 2;       // level starts
-        b = (b + 15) & ~size_t(15);
-        b += (size_t)MAXS * 4 * 2;       // FY scratch (keys + picked)
-        b += 64;
-        return b;
-    }
+struct SubStack {
+    uint64_t path;
+    int32_t parent_pre;  // -1: root / left child (no patch); else parent whose right child this is
+    uint32_t packed;     // start (10 bits) | n (11 bits) << 10 | rel depth (11 bits) << 21
 };
 
-template <typename T, int R>
-__device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, int ts, int D, uint64_t path,
-                          const DevCtx& c, uint32_t* fykeys, uint32_t* fypicked, int* fylock,
-                          int& out_dim, double& out_val, int& out_nl) {
-    typedef typename KeyOf<T>::type Key;
+constexpr int FY_SLOTS = 8192;  // global scratch slots for the rare exact-variance path
+
+__host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
+    size_t b = (size_t)dims * ts * tsize;
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)ts * 4;      // original row ids (the source buffer may be the output)
+    b += (size_t)2 * ts * 2;  // perm ping-pong by depth parity
+    b = (b + 15) & ~size_t(15);
+    b += 256 * 4;             // radix histogram
+    return b;
+}
+
+// k-th smallest key (0-based) of the node's values + below/equal counts and the
+// next larger key; keys striped in registers, 8-bit digit radix select with a
+// shared-memory histogram.
+template <int R, typename Key>
+__device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, uint32_t* hist, Key& ks, int& lt,
+                                            int& eq, Key& nxt) {
     const int lane = threadIdx.x & 31;
-    // per-dim: constant?, fast ssd + bound
-    double s2v[16], eb[16];
-    bool nonconst[16];
-    for (int d = 0; d < D; d++) {
+    constexpr int KB = sizeof(Key) * 8;
+    Key prefix = 0;
+    int rem = kth;
+#pragma unroll 1
+    for (int shift = KB - 8; shift >= 0; shift -= 8) {
+        for (int i = lane; i < 256; i += 32) hist[i] = 0;
+        __syncwarp();
+        const Key hmask = shift + 8 >= KB ? (Key)0 : (~(Key)0) << (shift + 8);
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int i = r * 32 + lane;
+            if (i < n && (kv[r] & hmask) == (prefix & hmask)) atomicAdd(&hist[(int)((kv[r] >> shift) & 255)], 1u);
+        }
+        __syncwarp();
+        // lane owns digits [8*lane, 8*lane+8)
+        uint32_t h[8];
+        uint32_t s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) { h[j] = hist[lane * 8 + j]; s += h[j]; }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - s;
+        const bool mine = (uint32_t)rem >= excl && (uint32_t)rem < incl;
+        int digit = 0, newrem = 0;
+        if (mine) {
+            uint32_t acc = excl;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if ((uint32_t)rem >= acc && (uint32_t)rem < acc + h[j]) { digit = lane * 8 + j; newrem = rem - (int)acc; }
+                acc += h[j];
+            }
+        }
+        const unsigned who = __ballot_sync(FULL, mine);
+        const int src = __ffs(who) - 1;
+        digit = __shfl_sync(FULL, digit, src);
+        rem = __shfl_sync(FULL, newrem, src);
+        prefix |= ((Key)digit) << shift;
+        __syncwarp();
+    }
+    ks = prefix;
+    int l = 0, e = 0;
+    Key nx = ~(Key)0;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int i = r * 32 + lane;
+        if (i < n) {
+            l += kv[r] < ks;
+            e += kv[r] == ks;
+            if (kv[r] > ks && kv[r] < nx) nx = kv[r];
+        }
+    }
+    lt = warp_isum(l);
+    eq = warp_isum(e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const Key on = __shfl_xor_sync(FULL, nx, o);
+        nx = on < nx ? on : nx;
+    }
+    nxt = nx;
+}
+
+template <typename T, int DT, int R>
+__device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, int ts, int dims_rt, uint64_t path,
+                          const DevCtx& c, uint32_t* hist, uint32_t* fyslots, int* fylocks, int& out_dim,
+                          double& out_val, int& out_nl) {
+    typedef typename KeyOf<T>::type Key;
+    constexpr int DC = DT > 0 ? DT : 16;
+    const int D = DT > 0 ? DT : dims_rt;
+    const int lane = threadIdx.x & 31;
+    double s2v[DC], eb[DC];
+    bool nonconst[DC];
+#pragma unroll
+    for (int d = 0; d < DC; d++) {
+        s2v[d] = 0.0; eb[d] = 0.0; nonconst[d] = false;
+        if (d >= D) continue;
         const T* row = cs + d * ts;
         double xs[R];
         Key kmn = ~(Key)0, kmx = 0;
@@ -767,6 +906,7 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
             s1 = __dadd_rn(s1, xs[r]);
             sa = __dadd_rn(sa, fabs(xs[r]));
         }
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const Key a = __shfl_xor_sync(FULL, kmn, o), b = __shfl_xor_sync(FULL, kmx, o);
             kmn = a < kmn ? a : kmn;
@@ -789,46 +929,53 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
         eb[d] = ssd_bound(s2v[d], sa, n);
     }
     int best = -1;
-    for (int d = 0; d < D; d++)
-        if (nonconst[d] && (best < 0 || s2v[d] > s2v[best])) best = d;
+    double bs = 0.0, be = 0.0;
+#pragma unroll
+    for (int d = 0; d < DC; d++)
+        if (nonconst[d] && (best < 0 || s2v[d] > bs)) { best = d; bs = s2v[d]; be = eb[d]; }
     out_dim = -1;
     if (best < 0) return;  // every dimension constant: degenerate leaf
     bool certified = true;
-    for (int d = 0; d < D; d++)
-        if (d != best && nonconst[d] && !(s2v[best] - s2v[d] > eb[best] + eb[d])) certified = false;
+#pragma unroll
+    for (int d = 0; d < DC; d++)
+        if (d != best && nonconst[d] && !(bs - s2v[d] > be + eb[d])) certified = false;
     if (!certified) {
-        // exact: Fisher-Yates order over the node (take == n) and sequential sums
-        if (lane == 0) while (atomicCAS(fylock, 0, 1) != 0) {}
+        // exact: the variance sample is the whole node in Fisher-Yates draw order
+        const int slot = blockIdx.x % FY_SLOTS;
+        if (lane == 0) while (atomicCAS(&fylocks[slot], 0, 1) != 0) {}
         __syncwarp();
-        __threadfence_block();
-        fy_resolve<R, uint32_t>((uint32_t)n, n, node_seed(c.seed, path, 0), fykeys, fypicked);
+        __threadfence();
+        uint32_t* fk = fyslots + (size_t)slot * 2 * MAXS;
+        uint32_t* fp = fk + MAXS;
+        fy_resolve<R, uint32_t>((uint32_t)n, n, node_seed(c.seed, path, 0), fk, fp);
         double exact = 0.0;
-        if (lane < D) {
+        if (lane < D && nonconst[lane < DC ? lane : 0]) {
             const T* row = cs + lane * ts;
             double mean = 0.0;
-            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[perm[start + fypicked[j]]]);
+            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[perm[start + fp[j]]]);
             mean = __ddiv_rn(mean, (double)n);
             double s = 0.0;
             for (int j = 0; j < n; j++) {
-                const double df = __dsub_rn((double)row[perm[start + fypicked[j]]], mean);
+                const double df = __dsub_rn((double)row[perm[start + fp[j]]], mean);
                 s = __dadd_rn(s, __dmul_rn(df, df));
             }
             exact = s;
         }
         __syncwarp();
-        __threadfence_block();
-        if (lane == 0) atomicExch(fylock, 0);
-        // first non-constant dimension in stable descending order
+        __threadfence();
+        if (lane == 0) atomicExch(&fylocks[slot], 0);
         best = -1;
         double bv = 0.0;
         for (int d = 0; d < D; d++) {
             const double e = __shfl_sync(FULL, exact, d);
-            if (!nonconst[d]) continue;
-            if (best < 0 || -e < -bv) { best = d; bv = e; }
+            bool nc = false;
+#pragma unroll
+            for (int dd = 0; dd < DC; dd++)
+                if (dd == d) nc = nonconst[dd];
+            if (!nc) continue;
+            if (best < 0 || -e < -bv) { best = d; bv = e; }  // stable descending (argsort(-ssd))
         }
     }
-    // exact median select over all n values (n <= sample size: boundaries = all
-    // distinct values; median.py:143-166 reduces to the two boundaries around n/2)
     const T* row = cs + best * ts;
     Key kv[R];
 #pragma unroll
@@ -836,25 +983,9 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
         const int i = r * 32 + lane;
         kv[r] = i < n ? tkey(row[perm[start + i]]) : ~(Key)0;
     }
-    warp_sort<R>(kv);
-    const Key ks = warp_get<R>(kv, n / 2);
-    int lt = 0, eq = 0;
-    Key nxt = ~(Key)0;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const int i = r * 32 + lane;
-        if (i < n) {
-            lt += kv[r] < ks;
-            eq += kv[r] == ks;
-            if (kv[r] > ks && kv[r] < nxt) nxt = kv[r];
-        }
-    }
-    lt = warp_isum(lt);
-    eq = warp_isum(eq);
-    for (int o = 16; o > 0; o >>= 1) {
-        const Key on = __shfl_xor_sync(FULL, nxt, o);
-        nxt = on < nxt ? on : nxt;
-    }
+    Key ks, nxt;
+    int lt, eq;
+    warp_select<R, Key>(kv, n, n / 2, hist, ks, lt, eq, nxt);
     const int cumA = lt, cumB = lt + eq;
     bool pickB;
     if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
@@ -865,42 +996,44 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
     out_nl = pickB ? cumB : cumA;
 }
 
-template <typename T>
+template <typename T, int DT>
 __device__ __forceinline__ void sub_split_dispatch(const T* cs, const uint16_t* perm, int start, int n, int ts, int D,
-                                                   uint64_t path, const DevCtx& c, uint32_t* fk, uint32_t* fp,
-                                                   int* lock, int& dim, double& val, int& nl) {
-    if (n <= 32) sub_split<T, 1>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
-    else if (n <= 64) sub_split<T, 2>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
-    else if (n <= 128) sub_split<T, 4>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
-    else if (n <= 256) sub_split<T, 8>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
-    else if (n <= 512) sub_split<T, 16>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
-    else sub_split<T, 32>(cs, perm, start, n, ts, D, path, c, fk, fp, lock, dim, val, nl);
+                                                   uint64_t path, const DevCtx& c, uint32_t* hist, uint32_t* fys,
+                                                   int* fyl, int& dim, double& val, int& nl) {
+    if (n <= 32) sub_split<T, DT, 1>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
+    else if (n <= 64) sub_split<T, DT, 2>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
+    else if (n <= 128) sub_split<T, DT, 4>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
+    else if (n <= 256) sub_split<T, DT, 8>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
+    else if (n <= 512) sub_split<T, DT, 16>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
+    else sub_split<T, DT, 32>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(SUB_THREADS)
+template <typename T, int DT>
+__global__ void __launch_bounds__(32, 12)
 k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0, const int32_t* idx1, DevCtx c,
-          KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, int32_t* task_nodes, int32_t* task_depth) {
+          KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, SubStack* __restrict__ sstack,
+          uint32_t* __restrict__ fyslots, int* __restrict__ fylocks, int32_t* task_nodes, int32_t* task_depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Task tk = tasks[blockIdx.x];
-    const int D = c.dims;
+    const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
     const int ts = c.ts;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const T* src = tk.src ? buf1 : buf0;
     const int32_t* isrc = tk.src ? idx1 : idx0;
     KdNode* out_nodes = scratch + 2 * tk.start;
     int32_t* out_cnt = scnt + 2 * tk.start;
+    SubStack* stk = sstack + 2 * tk.start;
 
     if (tk.leaf || tk.n > ts) {
         // degenerate leaf (possibly larger than the shared-memory limit): copy through
         if (tk.src) {
-            for (int64_t e = threadIdx.x; e < tk.n; e += blockDim.x) {
+            for (int64_t e = lane; e < tk.n; e += 32) {
                 for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = src[(int64_t)d * N + tk.start + e];
                 idx0[tk.start + e] = isrc[tk.start + e];
             }
         }
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             out_nodes[0] = KdNode{0.0, (int32_t)tk.start, -1 - tk.n};
             out_cnt[0] = tk.n;
             task_nodes[blockIdx.x] = 1;
@@ -909,176 +1042,88 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         return;
     }
     const int n = tk.n;
-    // ---- carve shared memory
     unsigned char* p = smem_raw;
     T* cs = reinterpret_cast<T*>(p); p += (size_t)D * ts * sizeof(T);
     p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
     int32_t* cidx = reinterpret_cast<int32_t*>(p); p += (size_t)ts * 4;
-    uint16_t* perm0 = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
-    uint16_t* perm1 = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
+    uint16_t* perm[2];
+    perm[0] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
+    perm[1] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
     p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
-    const int NS = 2 * ts + 2;
-    double* nv = reinterpret_cast<double*>(p); p += (size_t)NS * 8;
-    uint16_t* nstart = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    uint16_t* ncnt = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    uint16_t* nleft = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    uint16_t* nright = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    uint16_t* nsub = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    uint16_t* npre = reinterpret_cast<uint16_t*>(p); p += (size_t)NS * 2;
-    int8_t* ndim = reinterpret_cast<int8_t*>(p); p += (size_t)NS;
-    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
-    const int NL = ts / 2 + 2;
-    uint64_t* lpath0 = reinterpret_cast<uint64_t*>(p); p += (size_t)NL * 8;
-    uint64_t* lpath1 = reinterpret_cast<uint64_t*>(p); p += (size_t)NL * 8;
-    uint16_t* lslot0 = reinterpret_cast<uint16_t*>(p); p += (size_t)NL * 2;
-    uint16_t* lslot1 = reinterpret_cast<uint16_t*>(p); p += (size_t)NL * 2;
-    uint16_t* lvl = reinterpret_cast<uint16_t*>(p); p += (size_t)(ts + 2) * 2;
-    p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
-    uint32_t* fykeys = reinterpret_cast<uint32_t*>(p); p += (size_t)MAXS * 4;
-    uint32_t* fypicked = reinterpret_cast<uint32_t*>(p); p += (size_t)MAXS * 4;
-    int* misc = reinterpret_cast<int*>(p);  // [0]=slots [1]=next count [2]=lock [3]=maxlevel [4]=cur count
-    // ---- load the task's points
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    for (int e = lane; e < n; e += 32) {
         for (int d = 0; d < D; d++) cs[d * ts + e] = src[(int64_t)d * N + tk.start + e];
         cidx[e] = isrc[tk.start + e];
-        perm0[e] = (uint16_t)e;
+        perm[0][e] = (uint16_t)e;
     }
-    if (threadIdx.x == 0) {
-        misc[0] = 1; misc[1] = 0; misc[2] = 0; misc[3] = 0;
-        nstart[0] = 0; ncnt[0] = (uint16_t)n;
-        lvl[0] = 0; lvl[1] = 1;
-        if (n > c.bucket) { lslot0[0] = 0; lpath0[0] = tk.path; misc[4] = 1; }
-        else { ndim[0] = -1; misc[4] = 0; }
-    }
-    __syncthreads();
-    uint16_t* pc = perm0;
-    uint16_t* pn = perm1;
-    uint64_t* lpc = lpath0; uint64_t* lpn = lpath1;
-    uint16_t* lsc = lslot0; uint16_t* lsn = lslot1;
-    int level = 0;
-    // root leaf: emit
-    if (misc[4] == 0) {
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = cs[d * ts + e];
-            idx0[tk.start + e] = cidx[e];
+    __syncwarp();
+    auto emit = [&](const uint16_t* pm, int st, int len) {
+        for (int e = lane; e < len; e += 32) {
+            const int qv = pm[st + e];
+            for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + st + e] = cs[d * ts + qv];
+            idx0[tk.start + st + e] = cidx[qv];
         }
-    }
-    while (true) {
-        const int cnt = misc[4];
-        if (cnt == 0) break;
-        for (int li = warp; li < cnt; li += SUB_WARPS) {
-            const int slot = lsc[li];
-            const uint64_t path = lpc[li];
-            const int st = nstart[slot], nn = ncnt[slot];
-            int dim;
-            double val;
-            int nl;
-            sub_split_dispatch<T>(cs, pc, st, nn, ts, D, path, c, fykeys, fypicked, &misc[2], dim, val, nl);
-            if (dim < 0) {  // degenerate leaf
-                if (lane == 0) { ndim[slot] = -1; }
-                for (int e = lane; e < nn; e += 32) {
-                    const int q = pc[st + e];
-                    for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + st + e] = cs[d * ts + q];
-                    idx0[tk.start + st + e] = cidx[q];
-                }
-                continue;
-            }
-            // stable partition pc[st..st+nn) -> pn
-            int lrun = 0;
-            const T* row = cs + dim * ts;
-            for (int b = 0; b < nn; b += 32) {
-                const int e = b + lane;
-                const bool valid = e < nn;
-                const int q = valid ? pc[st + e] : 0;
-                const bool f = valid && (double)row[q] < val;
-                const unsigned bal = __ballot_sync(FULL, f);
-                const int lp = __popc(bal & ((1u << lane) - 1));
-                if (valid) {
-                    const int pos = f ? lrun + lp : nl + (e - (lrun + lp));
-                    pn[st + pos] = (uint16_t)q;
-                }
-                lrun += __popc(bal);
-            }
-            __syncwarp();
-            int cb = 0;
-            if (lane == 0) cb = atomicAdd(&misc[0], 2);
-            cb = __shfl_sync(FULL, cb, 0);
+    };
+    // depth-first, left child first: preorder numbering is the visit order
+    int cursor = 0, maxd = 0, sp = 0;
+    int st = 0, nn = n, rd = 0, parent_pre = -1;
+    uint64_t path = tk.path;
+    for (;;) {
+        const int pre = cursor++;
+        if (parent_pre >= 0 && lane == 0) out_nodes[parent_pre].a = pre;  // right child index
+        maxd = max(maxd, rd);
+        int dim = -1, nl = 0;
+        double val = 0.0;
+        if (nn > c.bucket) sub_split_dispatch<T, DT>(cs, perm[rd & 1], st, nn, ts, D, path, c, hist, fyslots, fylocks,
+                                                     dim, val, nl);
+        if (dim < 0) {
             if (lane == 0) {
-                ndim[slot] = (int8_t)dim;
-                nv[slot] = val;
-                nleft[slot] = (uint16_t)cb;
-                nright[slot] = (uint16_t)(cb + 1);
-                nstart[cb] = (uint16_t)st; ncnt[cb] = (uint16_t)nl;
-                nstart[cb + 1] = (uint16_t)(st + nl); ncnt[cb + 1] = (uint16_t)(nn - nl);
+                out_nodes[pre] = KdNode{0.0, (int32_t)(tk.start + st), -1 - nn};
+                out_cnt[pre] = nn;
             }
-            // children: push or emit
-            for (int k = 0; k < 2; k++) {
-                const int cst = k ? st + nl : st, cn = k ? nn - nl : nl;
-                if (cn > c.bucket) {
-                    if (lane == 0) {
-                        const int q = atomicAdd(&misc[1], 1);
-                        lsn[q] = (uint16_t)(cb + k);
-                        lpn[q] = path * 2ULL + (uint64_t)k;
-                    }
-                } else {
-                    if (lane == 0) ndim[cb + k] = -1;
-                    for (int e = lane; e < cn; e += 32) {
-                        const int q = pn[cst + e];
-                        for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + cst + e] = cs[d * ts + q];
-                        idx0[tk.start + cst + e] = cidx[q];
-                    }
-                }
-            }
+            emit(perm[rd & 1], st, nn);
+            if (sp == 0) break;
+            sp--;
+            const SubStack e = stk[sp];
+            path = e.path;
+            parent_pre = e.parent_pre;
+            st = (int)(e.packed & 1023u);
+            nn = (int)((e.packed >> 10) & 2047u);
+            rd = (int)(e.packed >> 21);
+            continue;
         }
-        __syncthreads();
-        level++;
-        if (threadIdx.x == 0) {
-            misc[4] = misc[1];
-            misc[1] = 0;
-            lvl[level + 1] = (uint16_t)misc[0];
-            misc[3] = level;
+        // stable partition into the other parity buffer
+        const uint16_t* pc = perm[rd & 1];
+        uint16_t* pn = perm[(rd + 1) & 1];
+        const T* row = cs + dim * ts;
+        int lrun = 0;
+        for (int b = 0; b < nn; b += 32) {
+            const int e = b + lane;
+            const bool valid = e < nn;
+            const int qv = valid ? pc[st + e] : 0;
+            const bool f = valid && (double)row[qv] < val;
+            const unsigned bal = __ballot_sync(FULL, f);
+            const int lp = __popc(bal & ((1u << lane) - 1));
+            if (valid) pn[st + (f ? lrun + lp : nl + (e - (lrun + lp)))] = (uint16_t)qv;
+            lrun += __popc(bal);
         }
-        __syncthreads();
-        { uint16_t* t = pc; pc = pn; pn = t; }
-        { uint64_t* t = lpc; lpc = lpn; lpn = t; }
-        { uint16_t* t = lsc; lsc = lsn; lsn = t; }
-        // nodes of the next level live in (new) pc; ranges of finished nodes are final
-    }
-    // levels: slots [lvl[L], lvl[L+1]) hold depth-L nodes, L in [0, nlev)
-    const int nlev = misc[3] + 1;
-    const int nslots = misc[0];
-    // bottom-up subtree sizes
-    for (int L = nlev - 1; L >= 0; L--) {
-        const int a = lvl[L], b = min((int)lvl[L + 1], nslots);
-        for (int s = a + threadIdx.x; s < b; s += blockDim.x)
-            nsub[s] = ndim[s] < 0 ? 1 : (uint16_t)(1 + nsub[nleft[s]] + nsub[nright[s]]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) npre[0] = 0;
-    __syncthreads();
-    for (int L = 0; L < nlev; L++) {
-        const int a = lvl[L], b = min((int)lvl[L + 1], nslots);
-        for (int s = a + threadIdx.x; s < b; s += blockDim.x) {
-            if (ndim[s] >= 0) {
-                npre[nleft[s]] = (uint16_t)(npre[s] + 1);
-                npre[nright[s]] = (uint16_t)(npre[s] + 1 + nsub[nleft[s]]);
-            }
+        __syncwarp();
+        if (lane == 0) {
+            out_nodes[pre] = KdNode{val, -1, dim};
+            out_cnt[pre] = nn;
+            stk[sp] = SubStack{path * 2ULL + 1ULL, pre,
+                               (uint32_t)(st + nl) | ((uint32_t)(nn - nl) << 10) | ((uint32_t)(rd + 1) << 21)};
         }
-        __syncthreads();
+        sp++;
+        path = path * 2ULL;
+        parent_pre = -1;
+        nn = nl;
+        rd = rd + 1;
+        __syncwarp();
     }
-    // deepest leaf depth: a node at level L has depth tk.depth + L
-    for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
-        const int q = npre[s];
-        if (ndim[s] >= 0) out_nodes[q] = KdNode{nv[s], (int32_t)npre[nright[s]], (int32_t)ndim[s]};
-        else out_nodes[q] = KdNode{0.0, (int32_t)(tk.start + nstart[s]), -1 - (int32_t)ncnt[s]};
-        out_cnt[q] = ncnt[s];
-    }
-    if (threadIdx.x == 0) {
-        task_nodes[blockIdx.x] = nsub[0];
-        // depth of the deepest node: last level that holds any slot
-        int L = nlev - 1;
-        while (L > 0 && lvl[L] >= nslots) L--;
-        task_depth[blockIdx.x] = tk.depth + L;
+    if (lane == 0) {
+        task_nodes[blockIdx.x] = cursor;
+        task_depth[blockIdx.x] = tk.depth + maxd;
     }
 }
 
@@ -1166,6 +1211,24 @@ static void dfree(void* p, cudaStream_t st) {
 // keep freed stream-ordered allocations in the pool across the per-level host
 // synchronisations (the default release threshold of 0 returns them to the
 // driver at every sync and re-maps them on the next level)
+// persistent pinned words for the per-level counter read-back (page-locking per build costs ms)
+static unsigned long long* pinned_counters(int device) {
+    static unsigned long long* p[64] = {nullptr};
+    if (!p[device]) KD_CUDA(cudaMallocHost(&p[device], 4 * sizeof(unsigned long long)));
+    return p[device];
+}
+
+// persistent per-device scratch for the rare exact-variance path of k_subtree
+static uint32_t* fy_slots(int device, cudaStream_t st) {
+    static uint32_t* slots[64] = {nullptr};
+    if (!slots[device]) {
+        const size_t words = (size_t)FY_SLOTS * 2 * MAXS + FY_SLOTS;
+        KD_CUDA(cudaMalloc(&slots[device], words * 4));
+        KD_CUDA(cudaMemsetAsync(slots[device] + (size_t)FY_SLOTS * 2 * MAXS, 0, FY_SLOTS * 4, st));
+    }
+    return slots[device];
+}
+
 void retain_pool(int device) {
     static bool done[64] = {false};
     if (device < 0 || device >= 64 || done[device]) return;
@@ -1177,9 +1240,21 @@ void retain_pool(int device) {
     done[device] = true;
 }
 
+struct HostTrace {
+    bool on = std::getenv("KDB_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what, int a = -1) {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[kdb] %9.3f ms  %s %d\n", ms, what, a);
+    }
+};
+
 template <typename T>
 void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const BuildCfg& cfg, cudaStream_t st,
                 KdTreeDev* out, BuildStats* stats) {
+    HostTrace tr;
+    tr.mark("enter");
     cudaEvent_t e0, e1;
     KD_CUDA(cudaEventCreate(&e0));
     KD_CUDA(cudaEventCreate(&e1));
@@ -1210,7 +1285,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     // shared-memory capacity caps the subtree size for wide / f64 points
     int dev_smem = 0;
     KD_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, out->device));
-    while (c.ts > 32 && SubSmem::bytes(c.ts, dims, sizeof(T)) > (size_t)dev_smem) c.ts /= 2;
+    while (c.ts > 32 && sub_smem_bytes(c.ts, dims, sizeof(T)) > (size_t)dev_smem) c.ts /= 2;
     c.ts = std::max<int>(c.ts, 1);
 
     T* buf[2] = {dalloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
@@ -1244,7 +1319,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     unsigned long long* next_ctr = dalloc<unsigned long long>(1, st);
     int* slow_count = dalloc<int>(1, st);
     unsigned long long* h_ctr = nullptr;
-    KD_CUDA(cudaMallocHost(&h_ctr, 2 * sizeof(unsigned long long)));
+    h_ctr = pinned_counters(out->device);
 
     std::vector<LNode*> levels;
     std::vector<int> level_k;
@@ -1318,8 +1393,17 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
-        k_scatter<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], idx[par], buf[1 - par], idx[1 - par], lv, K, c, split,
-                                                     tile_loff);
+#define KD_SCATTER(DTV, CHV)                                                                                   \
+    k_scatter<T, DTV, CHV><<<tiles, TILE_THREADS, 0, st>>>(buf[par], idx[par], buf[1 - par], idx[1 - par], lv, K, c, \
+                                                           split, tile_loff)
+        switch (dims) {
+            case 1: KD_SCATTER(1, 16); break;
+            case 2: KD_SCATTER(2, 16); break;
+            case 3: KD_SCATTER(3, 16); break;
+            case 4: KD_SCATTER(4, 8); break;
+            default: KD_SCATTER(0, 2); break;
+        }
+#undef KD_SCATTER
         LNode* next = dalloc<LNode>(2 * (size_t)K, st);
         KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long), st));
         k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, par, (int)ts_used, ts, next, next_ctr,
@@ -1330,6 +1414,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         int* h_slow = reinterpret_cast<int*>(&h_ctr[1]) + 1;
         KD_CUDA(cudaMemcpyAsync(h_slow, slow_count, sizeof(int), cudaMemcpyDeviceToHost, st));
         KD_CUDA(cudaStreamSynchronize(st));
+        tr.mark("level done", (int)levels.size());
         slow_total += *h_slow;
         ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
         dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st);
@@ -1342,6 +1427,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         if (K > 0) levels.push_back(next);
         else dfree(next, st);
     }
+    tr.mark("top phase done");
     const int ntasks = ntasks_known > 0 ? ntasks_known : 1;
     // subtree phase
     KdNode* scratch = dalloc<KdNode>(2 * (size_t)n + 2, st);
@@ -1349,10 +1435,19 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int32_t* task_nodes = dalloc<int32_t>(ntasks, st);
     int32_t* task_depth = dalloc<int32_t>(ntasks, st);
     int32_t* task_base = dalloc<int32_t>(ntasks, st);
-    const size_t sub_smem = SubSmem::bytes(c.ts, dims, sizeof(T));
-    KD_CUDA(cudaFuncSetAttribute(k_subtree<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
-    k_subtree<T><<<ntasks, SUB_THREADS, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt,
-                                                       task_nodes, task_depth);
+    const size_t sub_smem = sub_smem_bytes(c.ts, dims, sizeof(T));
+    SubStack* sstack = dalloc<SubStack>(2 * (size_t)n + 2, st);
+    uint32_t* fyslots = fy_slots(out->device, st);
+    int* fylocks = reinterpret_cast<int*>(fyslots + (size_t)FY_SLOTS * 2 * MAXS);
+    if (dims == 3) {
+        KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
+        k_subtree<T, 3><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt, sstack,
+                                                      fyslots, fylocks, task_nodes, task_depth);
+    } else {
+        KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
+        k_subtree<T, 0><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt, sstack,
+                                                      fyslots, fylocks, task_nodes, task_depth);
+    }
     KD_CUDA(cudaGetLastError());
     // top counts bottom-up, preorder top-down
     for (int L = (int)levels.size() - 1; L >= 0; L--)
@@ -1386,6 +1481,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     KD_CUDA(cudaMemcpyAsync(&hleaves, d_leaves, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     KD_CUDA(cudaEventRecord(e1, st));
     KD_CUDA(cudaStreamSynchronize(st));
+    tr.mark("finalize done");
     int64_t depth = 0;
     for (int i = 0; i < ntasks_known; i++) depth = std::max<int64_t>(depth, hdepth[i]);
     out->n_nodes = total_nodes;
@@ -1409,12 +1505,12 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     for (auto l : levels) dfree(l, st);
     ts_free(ts);
     dfree(tasks, st); dfree(task_ctr, st); dfree(next_ctr, st); dfree(slow_count, st);
-    dfree(scratch, st); dfree(scnt, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
+    dfree(scratch, st); dfree(scnt, st); dfree(sstack, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
     dfree(d_leaves, st);
-    cudaFreeHost(h_ctr);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     KD_CUDA(cudaStreamSynchronize(st));
+    tr.mark("exit");
 }
 
 void free_tree(KdTreeDev* t) {

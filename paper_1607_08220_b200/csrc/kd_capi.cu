@@ -319,6 +319,7 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.nq = nq;
         a.k = k;
         a.sort_queries = !(flags & KD_NO_SORT);
+        a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
         DevBuf bq, br, be, bd, bi, bc, bctr;
         if (dev_ptrs) {
             a.queries = queries; a.radii = radii; a.excl = exclude_ids;

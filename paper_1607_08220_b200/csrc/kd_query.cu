@@ -18,9 +18,12 @@
 //     bound >= r' and can lose an exact tie with a smaller id: SURVEY §8(a) Q5.)
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "kd_common.cuh"
 #include "kd_query.cuh"
 #include "kd_tree.cuh"
+#include "kd_warp.cuh"
 
 namespace kdb {
 
@@ -248,6 +251,216 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
     }
 }
 
+// ----------------------------------------------------------------------------
+// Persistent warps with dynamic query fetch.  Each lane runs its own exact
+// traversal (same bounds / admission rules as k_knn); when a lane finishes its
+// query it takes the next one from a warp-local pool of leaf-sorted queries,
+// refilled 64 at a time from a global counter.  This removes the tail
+// imbalance of one-query-per-thread warps (a warp otherwise waits for its
+// slowest query) while keeping neighbouring lanes on neighbouring queries.
+// ----------------------------------------------------------------------------
+template <typename T, int DT, int KM>
+__global__ void __launch_bounds__(128)
+k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
+              const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
+              const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
+              const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
+              int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
+    constexpr int DC = Dims<DT>::cap;
+    constexpr int POOL = 64;
+    const int D = DT > 0 ? DT : dims_rt;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1;
+
+    double q[DC];
+    double radius = 0.0;
+    uint64_t ex = ~0ULL;
+    const bool has_ex = excl != nullptr;
+    int64_t qi = -1;
+    int64_t c0 = 0, c1 = 0, c2 = 0;
+    double bd[KM];
+    uint64_t bi[KM];
+    int cnt = 0;
+    double kth_d = 0.0;
+    uint64_t kth_i = 0;
+    float off[DC];
+    int st_node[QCAP];
+    float st_off[QCAP][DC];
+    int sp = 0;
+    int node = -1;
+    long long pool_base = 0;
+    int pool_left = 0;
+    bool exhausted = false;
+
+    auto admissible = [&](float b) {
+        const double bb = (double)b;
+        return cnt < k ? bb < radius : bb <= kth_d;
+    };
+
+    for (;;) {
+        // ---- hand out queries to idle lanes
+        const bool need = node < 0;
+        const unsigned mneed = __ballot_sync(FULL, need);
+        if (mneed && !exhausted) {
+            int want = __popc(mneed);
+            int got_rank = -1;
+            // lanes take from the pool in lane order
+            int rank = __popc(mneed & lt_mask);
+            long long myq = -1;
+            if (rank < pool_left) myq = pool_base + rank;
+            const int taken = min(want, pool_left);
+            pool_base += taken;
+            pool_left -= taken;
+            if (want > taken) {
+                long long nb = 0;
+                if (lane == 0) nb = (long long)atomicAdd(counter, (unsigned long long)POOL);
+                nb = __shfl_sync(FULL, nb, 0);
+                if (nb >= nq) {
+                    exhausted = true;
+                } else {
+                    pool_base = nb;
+                    pool_left = (int)min((long long)POOL, nq - nb);
+                    const int r2 = rank - taken;
+                    if (need && r2 >= 0 && r2 < pool_left) myq = pool_base + r2;
+                    const int t2 = min(want - taken, pool_left);
+                    pool_base += t2;
+                    pool_left -= t2;
+                }
+            }
+            (void)got_rank;
+            if (need && myq >= 0 && myq < nq) {
+                qi = order ? (int64_t)order[myq] : myq;
+#pragma unroll
+                for (int d = 0; d < DC; d++) q[d] = d < D ? queries[qi * D + d] : 0.0;
+                radius = radii ? radii[qi] : INFINITY;
+                ex = has_ex ? excl[qi] : ~0ULL;
+                cnt = 0;
+                kth_d = radius;
+                kth_i = 0;
+                c0 = c1 = c2 = 0;
+                sp = 0;
+#pragma unroll
+                for (int d = 0; d < DC; d++) off[d] = 0.0f;
+                node = n_nodes > 0 ? 0 : -2;  // -2: finished immediately (empty tree)
+            }
+        }
+        if (node == -2) {
+            out_c[qi] = 0;
+            if (out_ctr) { out_ctr[qi * 3] = 0; out_ctr[qi * 3 + 1] = 0; out_ctr[qi * 3 + 2] = 0; }
+            node = -1;
+        }
+        if (__ballot_sync(FULL, node >= 0) == 0) {
+            if (exhausted) break;
+            continue;
+        }
+        if (node < 0) continue;
+        // ---- descend to a leaf, pushing admissible far children
+        for (;;) {
+            c0++;
+            const KdNode rec = nodes[node];
+            if (rec.db < 0) {
+                // ---- scan the bucket
+                const int start = rec.a, len = -1 - rec.db;
+                c1++;
+                c2 += len;
+                for (int i = start; i < start + len; i++) {
+                    double dist = 0.0;
+#pragma unroll
+                    for (int d = 0; d < DC; d++) {
+                        if (d < D) {
+                            const double df = __dsub_rn((double)coords[(int64_t)d * n + i], q[d]);
+                            dist = __dadd_rn(dist, __dmul_rn(df, df));
+                        }
+                    }
+                    if (cnt < k) {
+                        if (!(dist < radius)) continue;
+                    } else if (!(dist <= kth_d)) {
+                        continue;
+                    }
+                    const uint64_t id = ids[i];
+                    if (has_ex && id == ex) continue;
+                    if (cnt == k && !lexless(dist, id, kth_d, kth_i)) continue;
+                    const int p = cnt < k ? cnt : k - 1;
+#pragma unroll
+                    for (int j = 0; j < KM; j++)
+                        if (j == p) { bd[j] = dist; bi[j] = id; }
+#pragma unroll
+                    for (int j = KM - 1; j >= 1; j--) {
+                        if (j <= p && lexless(bd[j], bi[j], bd[j - 1], bi[j - 1])) {
+                            const double td = bd[j]; bd[j] = bd[j - 1]; bd[j - 1] = td;
+                            const uint64_t ti = bi[j]; bi[j] = bi[j - 1]; bi[j - 1] = ti;
+                        }
+                    }
+                    if (cnt < k) cnt++;
+                    if (cnt == k) {
+#pragma unroll
+                        for (int j = 0; j < KM; j++)
+                            if (j == k - 1) { kth_d = bd[j]; kth_i = bi[j]; }
+                    }
+                }
+                break;
+            }
+            const int dim = rec.db;
+            double qd = q[0];
+#pragma unroll
+            for (int d = 1; d < DC; d++)
+                if (d == dim) qd = q[d];
+            const bool goleft = qd < rec.v;
+            const int near = goleft ? node + 1 : rec.a;
+            const int far = goleft ? rec.a : node + 1;
+            const float ad = __double2float_rz(fabs(qd - rec.v));
+            float fo[DC];
+            float fb = 0.0f;
+#pragma unroll
+            for (int d = 0; d < DC; d++) {
+                fo[d] = (d == dim) ? ad : off[d];
+                if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
+            }
+            if (admissible(fb) && sp < QCAP) {
+                st_node[sp] = far;
+#pragma unroll
+                for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
+                sp++;
+            }
+            node = near;
+        }
+        // ---- next admissible far child, or finish
+        node = -1;
+        while (sp > 0) {
+            sp--;
+            float po[DC];
+            float pb = 0.0f;
+#pragma unroll
+            for (int d = 0; d < DC; d++) {
+                po[d] = st_off[sp][d];
+                if (d < D) pb = __fadd_rz(pb, __fmul_rz(po[d], po[d]));
+            }
+            if (admissible(pb)) {
+                node = st_node[sp];
+#pragma unroll
+                for (int d = 0; d < DC; d++) off[d] = po[d];
+                break;
+            }
+            c0++;
+        }
+        if (node < 0) {
+            out_c[qi] = cnt;
+#pragma unroll
+            for (int j = 0; j < KM; j++) {
+                if (j < cnt) {
+                    out_d[qi * (int64_t)k + j] = bd[j];
+                    out_i[qi * (int64_t)k + j] = bi[j];
+                }
+            }
+            if (out_ctr) {
+                out_ctr[qi * 3 + 0] = c0;
+                out_ctr[qi * 3 + 1] = c1;
+                out_ctr[qi * 3 + 2] = c2;
+            }
+        }
+    }
+}
+
 // leaf reached by descending with the tie rule (coord >= value goes right);
 // used as the sort key that makes each warp's 32 queries spatially coherent
 template <int DT>
@@ -272,6 +485,24 @@ template <typename T, int DT, int KM>
 static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st) {
     const int threads = 128;
     const unsigned blocks = (unsigned)((a.nq + threads - 1) / threads);
+    if constexpr (KM > 0) {
+        if (!a.thread_per_query) {
+            int dev = 0, sms = 148, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_persist<T, DT, KM>, threads, 0);
+            const long long want = (a.nq + threads - 1) / threads;
+            const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
+            unsigned long long* ctr = nullptr;
+            KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
+            KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+            k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
+                t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
+                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
+            cudaFreeAsync(ctr, st);
+            return;
+        }
+    }
     k_knn<T, DT, KM><<<blocks, threads, 0, st>>>(t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n,
                                                  t.dims, a.queries, order, a.nq, (int)a.k, a.radii, a.excl, a.out_d,
                                                  a.out_i, a.out_c, a.out_ctr, a.heap_d, a.heap_i);

@@ -21,7 +21,7 @@ __all__ = ["find_knn", "find_knn_batch", "count_visited", "find_knn_device"]
 
 
 def find_knn_batch(tree: LocalTree, queries, k: int, radii=np.inf, workers: int = 1, *,
-                   exclude_ids=None, counters: bool = True, device: int = 0):
+                   exclude_ids=None, counters: bool = True, device: int = 0, flags: int = 0):
     """Exact KNN for a block of queries against one tree.
 
     Returns (dists (nq,k) f64, ids (nq,k) u64, counts (nq,) i64, counters (nq,3) i64);
@@ -59,7 +59,7 @@ def find_knn_batch(tree: LocalTree, queries, k: int, radii=np.inf, workers: int 
     nt = tree.native(device)
     N.check(N.lib.kd_knn(nt.handle, q.ctypes.data, nq, k, None if r is None else r.ctypes.data,
                          None if ex is None else ex.ctypes.data, out_d.ctypes.data, out_i.ctypes.data,
-                         out_c.ctypes.data, out_ctr.ctypes.data if counters else None, 0, None))
+                         out_c.ctypes.data, out_ctr.ctypes.data if counters else None, flags, None))
     return out_d, out_i, out_c, out_ctr
 
 
@@ -81,7 +81,7 @@ def count_visited(tree: LocalTree, q, k: int, sq_radius: float = np.inf) -> dict
 
 
 def find_knn_device(tree: LocalTree, queries, k: int, radii=None, exclude_ids=None, counters: bool = False,
-                    sort_queries: bool = True, stream=None, out=None):
+                    sort_queries: bool = True, stream=None, out=None, flags: int = 0):
     """Device-tensor variant: queries (nq, dims) float64 CUDA tensor.  Returns
     torch tensors (dists, ids(int64 view of uint64), counts, counters|None)."""
     import torch
@@ -98,7 +98,7 @@ def find_knn_device(tree: LocalTree, queries, k: int, radii=None, exclude_ids=No
     else:
         od, oi, oc, octr = out
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    flags = N.KD_DEVICE_PTRS | (0 if sort_queries else N.KD_NO_SORT)
+    flags = flags | N.KD_DEVICE_PTRS | (0 if sort_queries else N.KD_NO_SORT)
     nt = tree.native(dev.index or 0)
     N.check(N.lib.kd_knn(nt.handle, queries.data_ptr(), nq, k,
                          radii.data_ptr() if radii is not None else None,
