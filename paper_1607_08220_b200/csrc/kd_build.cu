@@ -104,11 +104,12 @@ __device__ __forceinline__ double ssd_bound(double s2, double sabs, int t) {
 // ============================================================================
 // k_sample: one warp per breadth-first node
 // ============================================================================
-template <typename T>
+template <typename T, int DT>
 __global__ void __launch_bounds__(SAMPLE_WARPS * 32)
 k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
          T* __restrict__ wb, uint32_t* __restrict__ wf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int DC = DT > 0 ? DT : 16;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ni = blockIdx.x * SAMPLE_WARPS + warp;
     if (ni >= K) return;
@@ -116,7 +117,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * 8) + warp * MAXS;
     const LNode nd = nodes[ni];
     const uint32_t n = (uint32_t)nd.n;
-    const int D = c.dims;
+    const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
 
     // --- variance sample (local_tree.py:122-132)
@@ -125,39 +126,39 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     if (n <= (1u << 22)) fy_resolve<32, uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(skeys), picked);
     else fy_resolve<32, uint64_t>(n, take, vseed, skeys, picked);
 
-    double s2v[16], eb[16];
-    for (int d = 0; d < D; d++) {
-        const T* row = src + (int64_t)d * N + nd.start;
-        double xs[32];
-        double s1 = 0.0, sa = 0.0;
+    int d0 = 0;
+    double b0 = 0.0, e0 = 0.0;
+    double s2v[DC], eb[DC];
 #pragma unroll
-        for (int r = 0; r < 32; r++) {
-            const int j = r * 32 + lane;
-            xs[r] = j < take ? (double)row[picked[j]] : 0.0;
-            s1 = __dadd_rn(s1, xs[r]);
-            sa = __dadd_rn(sa, fabs(xs[r]));
+    for (int d = 0; d < DC; d++) {
+        s2v[d] = 0.0;
+        eb[d] = 0.0;
+        if (d >= D) continue;
+        const T* row = src + (int64_t)d * N + nd.start;
+        double s1 = 0.0, sa = 0.0;
+#pragma unroll 4
+        for (int j = lane; j < take; j += 32) {
+            const double x = (double)row[picked[j]];
+            s1 = __dadd_rn(s1, x);
+            sa = __dadd_rn(sa, fabs(x));
         }
         s1 = warp_sum(s1);
         sa = warp_sum(sa);
         const double mean = __ddiv_rn(s1, (double)take);
         double s2 = 0.0;
-#pragma unroll
-        for (int r = 0; r < 32; r++) {
-            const int j = r * 32 + lane;
-            if (j < take) {
-                const double df = __dsub_rn(xs[r], mean);
-                s2 = __dadd_rn(s2, __dmul_rn(df, df));
-            }
+#pragma unroll 4
+        for (int j = lane; j < take; j += 32) {
+            const double df = __dsub_rn((double)row[picked[j]], mean);
+            s2 = __dadd_rn(s2, __dmul_rn(df, df));
         }
         s2v[d] = warp_sum(s2);
         eb[d] = ssd_bound(s2v[d], sa, take);
+        if (d == 0 || s2v[d] > b0) { d0 = d; b0 = s2v[d]; e0 = eb[d]; }
     }
-    int d0 = 0;
-    for (int d = 1; d < D; d++)
-        if (s2v[d] > s2v[d0]) d0 = d;
     bool certified = true;
-    for (int d = 0; d < D; d++)
-        if (d != d0 && !(s2v[d0] - s2v[d] > eb[d0] + eb[d])) certified = false;
+#pragma unroll
+    for (int d = 0; d < DC; d++)
+        if (d < D && d != d0 && !(b0 - s2v[d] > e0 + eb[d])) certified = false;
     if (!certified) {
         // exact sequential recomputation in draw order (rare: near-ties)
         double exact = 0.0;
@@ -197,11 +198,25 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     }
     warp_sort<32>(kv);
     // np.unique: first element of each run of equal keys; boundary index = rank of run
-    int nb_run = 0, cle = 0;
     const int mid = m / 2;
+    int nb = 0, cle = 0;
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+        const int s = r * 32 + lane;
+        Key prev = __shfl_up_sync(FULL, kv[r], 1);
+        const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
+        if (lane == 0) prev = lp;
+        const bool first = s < m && (s == 0 || kv[r] != prev);
+        nb += __popc(__ballot_sync(FULL, first));
+        cle += __popc(__ballot_sync(FULL, first && s <= mid));  // run holding sorted position `mid`
+    }
+    const int center = cle - 1;
+    int wlo = max(0, center - WIN / 2);
+    const int whi = min(nb, wlo + WIN);
+    wlo = max(0, whi - WIN);
     Split* sp = split + ni;
     T* wbn = wb + (int64_t)ni * WIN;
-    int bidx[32];
+    int run = 0;
 #pragma unroll
     for (int r = 0; r < 32; r++) {
         const int s = r * 32 + lane;
@@ -210,19 +225,9 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
         if (lane == 0) prev = lp;
         const bool first = s < m && (s == 0 || kv[r] != prev);
         const unsigned bal = __ballot_sync(FULL, first);
-        bidx[r] = first ? nb_run + __popc(bal & ((1u << lane) - 1)) : -1;
-        nb_run += __popc(bal);
-        // boundary (run) containing sorted position `mid`
-        cle += __popc(__ballot_sync(FULL, first && s <= mid));
-    }
-    const int center = cle - 1;
-    const int nb = nb_run;
-    int wlo = max(0, center - WIN / 2);
-    const int whi = min(nb, wlo + WIN);
-    wlo = max(0, whi - WIN);
-#pragma unroll
-    for (int r = 0; r < 32; r++) {
-        if (bidx[r] >= wlo && bidx[r] < whi) wbn[bidx[r] - wlo] = key_inv(kv[r], (T*)nullptr);
+        const int bi = run + __popc(bal & ((1u << lane) - 1));
+        if (first && bi >= wlo && bi < whi) wbn[bi - wlo] = key_inv(kv[r], (T*)nullptr);
+        run += __popc(bal);
     }
     uint32_t* wfn = wf + (int64_t)ni * WIN;
     for (int i = lane; i < WIN; i += 32) wfn[i] = 0;
@@ -802,11 +807,14 @@ __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
 }
 
 // k-th smallest key (0-based) of the node's values + below/equal counts and the
-// next larger key; keys striped in registers, 8-bit digit radix select with a
-// shared-memory histogram.
-template <int R, typename Key>
-__device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, uint32_t* hist, Key& ks, int& lt,
-                                            int& eq, Key& nxt) {
+// next larger key.  Keys are read from shared memory through the node's
+// permutation (runtime loops: small code, few registers); 8-bit digit radix
+// select with a per-warp shared-memory histogram.
+template <typename T>
+__device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, int n, int kth, uint32_t* hist,
+                                            typename KeyOf<T>::type& ks, int& lt, int& eq,
+                                            typename KeyOf<T>::type& nxt) {
+    typedef typename KeyOf<T>::type Key;
     const int lane = threadIdx.x & 31;
     constexpr int KB = sizeof(Key) * 8;
     Key prefix = 0;
@@ -816,13 +824,12 @@ __device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, 
         for (int i = lane; i < 256; i += 32) hist[i] = 0;
         __syncwarp();
         const Key hmask = shift + 8 >= KB ? (Key)0 : (~(Key)0) << (shift + 8);
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int i = r * 32 + lane;
-            if (i < n && (kv[r] & hmask) == (prefix & hmask)) atomicAdd(&hist[(int)((kv[r] >> shift) & 255)], 1u);
+#pragma unroll 4
+        for (int i = lane; i < n; i += 32) {
+            const Key kk = tkey(row[pm[i]]);
+            if ((kk & hmask) == (prefix & hmask)) atomicAdd(&hist[(int)((kk >> shift) & 255)], 1u);
         }
         __syncwarp();
-        // lane owns digits [8*lane, 8*lane+8)
         uint32_t h[8];
         uint32_t s = 0;
 #pragma unroll
@@ -844,8 +851,7 @@ __device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, 
                 acc += h[j];
             }
         }
-        const unsigned who = __ballot_sync(FULL, mine);
-        const int src = __ffs(who) - 1;
+        const int src = __ffs(__ballot_sync(FULL, mine)) - 1;
         digit = __shfl_sync(FULL, digit, src);
         rem = __shfl_sync(FULL, newrem, src);
         prefix |= ((Key)digit) << shift;
@@ -854,14 +860,12 @@ __device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, 
     ks = prefix;
     int l = 0, e = 0;
     Key nx = ~(Key)0;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const int i = r * 32 + lane;
-        if (i < n) {
-            l += kv[r] < ks;
-            e += kv[r] == ks;
-            if (kv[r] > ks && kv[r] < nx) nx = kv[r];
-        }
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+        const Key kk = tkey(row[pm[i]]);
+        l += kk < ks;
+        e += kk == ks;
+        if (kk > ks && kk < nx) nx = kk;
     }
     lt = warp_isum(l);
     eq = warp_isum(e);
@@ -873,38 +877,44 @@ __device__ __forceinline__ void warp_select(const Key (&kv)[R], int n, int kth, 
     nxt = nx;
 }
 
-template <typename T, int DT, int R>
-__device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, int ts, int dims_rt, uint64_t path,
+__device__ __noinline__ void fy_resolve_n(uint32_t n, uint64_t seed, uint32_t* fk, uint32_t* fp) {
+    if (n <= 32) fy_resolve<1, uint32_t>(n, (int)n, seed, fk, fp);
+    else if (n <= 64) fy_resolve<2, uint32_t>(n, (int)n, seed, fk, fp);
+    else if (n <= 128) fy_resolve<4, uint32_t>(n, (int)n, seed, fk, fp);
+    else if (n <= 256) fy_resolve<8, uint32_t>(n, (int)n, seed, fk, fp);
+    else if (n <= 512) fy_resolve<16, uint32_t>(n, (int)n, seed, fk, fp);
+    else fy_resolve<32, uint32_t>(n, (int)n, seed, fk, fp);
+}
+
+template <typename T, int DT>
+__device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int dims_rt, uint64_t path,
                           const DevCtx& c, uint32_t* hist, uint32_t* fyslots, int* fylocks, int& out_dim,
                           double& out_val, int& out_nl) {
     typedef typename KeyOf<T>::type Key;
     constexpr int DC = DT > 0 ? DT : 16;
     const int D = DT > 0 ? DT : dims_rt;
     const int lane = threadIdx.x & 31;
+    // per dimension: constant?, binary64 sum of squared deviations + bound
+    int best = -1;
+    double bs = 0.0, be = 0.0;
     double s2v[DC], eb[DC];
-    bool nonconst[DC];
+    unsigned ncmask = 0;
 #pragma unroll
     for (int d = 0; d < DC; d++) {
-        s2v[d] = 0.0; eb[d] = 0.0; nonconst[d] = false;
+        s2v[d] = 0.0;
+        eb[d] = 0.0;
         if (d >= D) continue;
         const T* row = cs + d * ts;
-        double xs[R];
         Key kmn = ~(Key)0, kmx = 0;
         double s1 = 0.0, sa = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int i = r * 32 + lane;
-            if (i < n) {
-                const T v = row[perm[start + i]];
-                xs[r] = (double)v;
-                const Key k = tkey(v);
-                kmn = k < kmn ? k : kmn;
-                kmx = k > kmx ? k : kmx;
-            } else {
-                xs[r] = 0.0;
-            }
-            s1 = __dadd_rn(s1, xs[r]);
-            sa = __dadd_rn(sa, fabs(xs[r]));
+#pragma unroll 4
+        for (int i = lane; i < n; i += 32) {
+            const T v = row[pm[i]];
+            const Key k = tkey(v);
+            kmn = k < kmn ? k : kmn;
+            kmx = k > kmx ? k : kmx;
+            s1 = __dadd_rn(s1, (double)v);
+            sa = __dadd_rn(sa, fabs((double)v));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -912,33 +922,27 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
             kmn = a < kmn ? a : kmn;
             kmx = b > kmx ? b : kmx;
         }
-        nonconst[d] = kmn != kmx;
+        if (kmn == kmx) continue;
+        ncmask |= 1u << d;
         s1 = warp_sum(s1);
         sa = warp_sum(sa);
         const double mean = __ddiv_rn(s1, (double)n);
         double s2 = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const int i = r * 32 + lane;
-            if (i < n) {
-                const double df = __dsub_rn(xs[r], mean);
-                s2 = __dadd_rn(s2, __dmul_rn(df, df));
-            }
+#pragma unroll 4
+        for (int i = lane; i < n; i += 32) {
+            const double df = __dsub_rn((double)row[pm[i]], mean);
+            s2 = __dadd_rn(s2, __dmul_rn(df, df));
         }
         s2v[d] = warp_sum(s2);
         eb[d] = ssd_bound(s2v[d], sa, n);
+        if (best < 0 || s2v[d] > bs) { best = d; bs = s2v[d]; be = eb[d]; }
     }
-    int best = -1;
-    double bs = 0.0, be = 0.0;
-#pragma unroll
-    for (int d = 0; d < DC; d++)
-        if (nonconst[d] && (best < 0 || s2v[d] > bs)) { best = d; bs = s2v[d]; be = eb[d]; }
     out_dim = -1;
     if (best < 0) return;  // every dimension constant: degenerate leaf
     bool certified = true;
 #pragma unroll
     for (int d = 0; d < DC; d++)
-        if (d != best && nonconst[d] && !(bs - s2v[d] > be + eb[d])) certified = false;
+        if (d != best && ((ncmask >> d) & 1u) && !(bs - s2v[d] > be + eb[d])) certified = false;
     if (!certified) {
         // exact: the variance sample is the whole node in Fisher-Yates draw order
         const int slot = blockIdx.x % FY_SLOTS;
@@ -947,16 +951,16 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
         __threadfence();
         uint32_t* fk = fyslots + (size_t)slot * 2 * MAXS;
         uint32_t* fp = fk + MAXS;
-        fy_resolve<R, uint32_t>((uint32_t)n, n, node_seed(c.seed, path, 0), fk, fp);
+        fy_resolve_n((uint32_t)n, node_seed(c.seed, path, 0), fk, fp);
         double exact = 0.0;
-        if (lane < D && nonconst[lane < DC ? lane : 0]) {
+        if (lane < D && ((ncmask >> lane) & 1u)) {
             const T* row = cs + lane * ts;
             double mean = 0.0;
-            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[perm[start + fp[j]]]);
+            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[pm[fp[j]]]);
             mean = __ddiv_rn(mean, (double)n);
             double s = 0.0;
             for (int j = 0; j < n; j++) {
-                const double df = __dsub_rn((double)row[perm[start + fp[j]]], mean);
+                const double df = __dsub_rn((double)row[pm[fp[j]]], mean);
                 s = __dadd_rn(s, __dmul_rn(df, df));
             }
             exact = s;
@@ -968,24 +972,13 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
         double bv = 0.0;
         for (int d = 0; d < D; d++) {
             const double e = __shfl_sync(FULL, exact, d);
-            bool nc = false;
-#pragma unroll
-            for (int dd = 0; dd < DC; dd++)
-                if (dd == d) nc = nonconst[dd];
-            if (!nc) continue;
+            if (!((ncmask >> d) & 1u)) continue;
             if (best < 0 || -e < -bv) { best = d; bv = e; }  // stable descending (argsort(-ssd))
         }
     }
-    const T* row = cs + best * ts;
-    Key kv[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const int i = r * 32 + lane;
-        kv[r] = i < n ? tkey(row[perm[start + i]]) : ~(Key)0;
-    }
     Key ks, nxt;
     int lt, eq;
-    warp_select<R, Key>(kv, n, n / 2, hist, ks, lt, eq, nxt);
+    warp_select<T>(cs + best * ts, pm, n, n / 2, hist, ks, lt, eq, nxt);
     const int cumA = lt, cumB = lt + eq;
     bool pickB;
     if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
@@ -994,18 +987,6 @@ __device__ void sub_split(const T* cs, const uint16_t* perm, int start, int n, i
     out_dim = best;
     out_val = pickB ? (double)key_inv(nxt, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
     out_nl = pickB ? cumB : cumA;
-}
-
-template <typename T, int DT>
-__device__ __forceinline__ void sub_split_dispatch(const T* cs, const uint16_t* perm, int start, int n, int ts, int D,
-                                                   uint64_t path, const DevCtx& c, uint32_t* hist, uint32_t* fys,
-                                                   int* fyl, int& dim, double& val, int& nl) {
-    if (n <= 32) sub_split<T, DT, 1>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
-    else if (n <= 64) sub_split<T, DT, 2>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
-    else if (n <= 128) sub_split<T, DT, 4>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
-    else if (n <= 256) sub_split<T, DT, 8>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
-    else if (n <= 512) sub_split<T, DT, 16>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
-    else sub_split<T, DT, 32>(cs, perm, start, n, ts, D, path, c, hist, fys, fyl, dim, val, nl);
 }
 
 template <typename T, int DT>
@@ -1074,8 +1055,8 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         maxd = max(maxd, rd);
         int dim = -1, nl = 0;
         double val = 0.0;
-        if (nn > c.bucket) sub_split_dispatch<T, DT>(cs, perm[rd & 1], st, nn, ts, D, path, c, hist, fyslots, fylocks,
-                                                     dim, val, nl);
+        if (nn > c.bucket) sub_split<T, DT>(cs, perm[rd & 1] + st, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val,
+                                            nl);
         if (dim < 0) {
             if (lane == 0) {
                 out_nodes[pre] = KdNode{0.0, (int32_t)(tk.start + st), -1 - nn};
@@ -1351,7 +1332,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     {
     }
     size_t sample_smem = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
-    KD_CUDA(cudaFuncSetAttribute(k_sample<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
     while (K > 0) {
@@ -1383,8 +1365,12 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         uint32_t* tile_left = dalloc<uint32_t>(tiles + 1, st);
         uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
         KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
-        k_sample<T><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
-            buf[par], lv, K, c, split, wb, wf);
+        if (dims == 3)
+            k_sample<T, 3><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
+                buf[par], lv, K, c, split, wb, wf);
+        else
+            k_sample<T, 0><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
+                buf[par], lv, K, c, split, wb, wf);
         k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, wb, wf);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(buf[par], lv, c, split, slow_list, slow_count);
