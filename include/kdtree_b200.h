@@ -126,6 +126,28 @@ KD_API int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k
 
 KD_API int kd_tree_free(kd_tree* t);
 
+/* ---- global (multi-GPU) tier, cluster.py / dist_query.py ---------------- */
+
+/* histogram_with_equals (median.py:243-265, cluster.py:246): counts[nb+1] of
+ * values by "number of boundaries <= v" and equals[nb] exact matches.
+ * boundaries sorted distinct binary64, 1 <= nb <= 4096. */
+KD_API int kd_histogram(const void* values, int dtype, int64_t n, const double* boundaries, int64_t nb,
+                        int64_t* counts, int64_t* equals, unsigned flags, void* stream);
+
+/* redistribute side split (cluster.py:292-294): stable two-way partition of a
+ * rank's SoA points + ids, coord[dim] < value first.  Device pointers only. */
+KD_API int kd_partition(const void* coords, int dtype, int64_t n, int dims, const uint64_t* ids, int dim,
+                        double value, void* out_coords, uint64_t* out_ids, int64_t* n_low, unsigned flags,
+                        void* stream);
+
+/* GlobalTree.owner_of_batch + ranks_within (cluster.py:96-154): owner rank of
+ * each query (ties right) and, when `within` is non-NULL, the bitmask of other
+ * ranks whose region's min squared distance is strictly below radii[i]
+ * (NULL = +inf).  Regions are [ranks][dims] lower/upper bounds.  Device ptrs. */
+KD_API int kd_route(const int32_t* plane_dims, const double* plane_values, int32_t ranks, const double* region_lo,
+                    const double* region_hi, const double* queries, int64_t nq, int dims, const double* radii,
+                    int32_t* owner, uint64_t* within, unsigned flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

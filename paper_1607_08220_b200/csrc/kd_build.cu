@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "kd_common.cuh"
@@ -1193,15 +1194,19 @@ static void dfree(void* p, cudaStream_t st) {
 // synchronisations (the default release threshold of 0 returns them to the
 // driver at every sync and re-maps them on the next level)
 // persistent pinned words for the per-level counter read-back (page-locking per build costs ms)
-static unsigned long long* pinned_counters(int device) {
-    static unsigned long long* p[64] = {nullptr};
-    if (!p[device]) KD_CUDA(cudaMallocHost(&p[device], 4 * sizeof(unsigned long long)));
-    return p[device];
+// (one per host thread: concurrent builds from several rank threads must not share it)
+static unsigned long long* pinned_counters(int) {
+    static thread_local unsigned long long* p = nullptr;
+    if (!p) KD_CUDA(cudaMallocHost(&p, 4 * sizeof(unsigned long long)));
+    return p;
 }
+
+static std::mutex g_init_mu;
 
 // persistent per-device scratch for the rare exact-variance path of k_subtree
 static uint32_t* fy_slots(int device, cudaStream_t st) {
     static uint32_t* slots[64] = {nullptr};
+    std::lock_guard<std::mutex> lk(g_init_mu);
     if (!slots[device]) {
         const size_t words = (size_t)FY_SLOTS * 2 * MAXS + FY_SLOTS;
         KD_CUDA(cudaMalloc(&slots[device], words * 4));
@@ -1212,6 +1217,7 @@ static uint32_t* fy_slots(int device, cudaStream_t st) {
 
 void retain_pool(int device) {
     static bool done[64] = {false};
+    std::lock_guard<std::mutex> lk(g_init_mu);
     if (device < 0 || device >= 64 || done[device]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

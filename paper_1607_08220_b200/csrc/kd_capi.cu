@@ -25,6 +25,8 @@ static int fail(int code, const std::string& msg) {
     return code;
 }
 
+int kd_set_error(int code, const char* msg) { return fail(code, msg); }
+
 #define KD_TRY(...)                                                                    \
     try {                                                                              \
         __VA_ARGS__;                                                                        \

@@ -105,3 +105,28 @@ def big_cases():
     q = np.random.default_rng(80).random((300, 10), dtype=np.float32).astype(np.float64)
     out["f32_u10_100k_b64"] = (np.ascontiguousarray(rows.T), dict(bucket_size=64, seed=12), q, 10)
     return out
+
+
+def engine_cases():
+    """Multi-rank cases for build_engine / Engine.query: name -> (rows, RunConfig kwargs, queries, k)."""
+    out = {}
+
+    def q_for(rows, seed, nq=300):
+        rng = np.random.default_rng(seed)
+        lo, hi = rows.min(0), rows.max(0)
+        return np.concatenate([rng.uniform(lo, hi, size=(nq - 50, rows.shape[1])), rows[:50]])
+
+    rows = make_rows(20000, 3, 5)
+    out["eng_u3_20000_p4"] = (rows, dict(ranks=4, seed=5), q_for(rows, 1), 5)
+    out["eng_u3_20000_p8"] = (rows, dict(ranks=8, seed=6), q_for(rows, 2), 5)
+    rows = make_rows(50000, 3, 11, "f32")
+    out["eng_f32_50000_p2"] = (rows, dict(ranks=2, seed=11), q_for(rows, 3), 6)
+    rows = make_rows(2000, 2, 9, "duplicate-heavy")
+    out["eng_dup2_2000_p4"] = (rows, dict(ranks=4, seed=9), q_for(rows, 4), 3)
+    rows = make_rows(5000, 3, 13)
+    out["eng_u3_5000_p16"] = (rows, dict(ranks=16, seed=13, batch_size=64), q_for(rows, 5), 5)
+    rows = make_rows(40000, 3, 17, "halo-f32")
+    out["eng_halo_40000_p8"] = (rows, dict(ranks=8, seed=2, bucket_size=16), q_for(rows, 6), 5)
+    rows = make_rows(6000, 10, 19)
+    out["eng_d10_6000_p4"] = (rows, dict(ranks=4, seed=3, bucket_size=64), q_for(rows, 7, 100), 7)
+    return out

@@ -42,7 +42,7 @@ from conftest import oracle_topk  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
-from datagen import golden_cases, big_cases  # noqa: E402
+from datagen import golden_cases, big_cases, engine_cases  # noqa: E402
 
 
 def tree_arrays(tree):
@@ -145,7 +145,33 @@ def big():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def engine():
+    """build_engine + Engine.query (engine.py:159-217) -> bundle digest, counters, results."""
+    from kdknn.engine import RunConfig, build_engine, bundle_to_bytes
+    out, arrays = {}, {}
+    for name, (rows, cfg, queries, k) in engine_cases().items():
+        ps = PointSet.from_rows(rows)
+        eng, rep = build_engine(ps, RunConfig(**cfg))
+        blob = bundle_to_bytes(eng)
+        res, qrep = eng.query(queries, k=k)
+        d = np.array([[n.sq_dist for n in r.neighbors] for r in res])
+        i = np.array([[n.point_id for n in r.neighbors] for r in res], dtype=np.uint64)
+        arrays[f"{name}/dists"] = d
+        arrays[f"{name}/ids"] = i
+        out[name] = {"bundle_sha256": hashlib.sha256(blob).hexdigest(), "bundle_len": len(blob),
+                     "global_tree": eng.ranks[0].global_tree.to_bytes().hex(), "points_moved": rep.points_moved,
+                     "rank_counts": [int(r.points.count) for r in eng.ranks],
+                     "queries_forwarded": qrep.queries_forwarded, "requests_sent": qrep.requests_sent,
+                     "requests_received": qrep.requests_received, "soundness_violations": qrep.soundness_violations,
+                     "nodes_visited": qrep.nodes_visited, "points_compared": qrep.points_compared}
+        print(f"  engine {name}: forwarded={qrep.queries_forwarded} moved={rep.points_moved}")
+    with open(os.path.join(HERE, "engine.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    np.savez_compressed(os.path.join(HERE, "engine_knn.npz"), **arrays)
+
+
 if __name__ == "__main__":
     primitives()
     trees_and_knn()
     big()
+    engine()
