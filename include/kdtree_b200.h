@@ -57,7 +57,6 @@ extern "C" {
 #define KD_DEVICE_PTRS 1u     /* all array arguments are device pointers */
 #define KD_NO_SORT 2u         /* kd_knn: keep caller query order (no leaf sort) */
 #define KD_THREAD_PER_QUERY 4u /* kd_knn: one thread per query, no dynamic fetch (default: persistent warps) */
-#define KD_WARP_SERVED 8u      /* kd_knn: experimental warp-served leaf kernel (default: persistent warps) */
 
 typedef struct kd_tree kd_tree;
 

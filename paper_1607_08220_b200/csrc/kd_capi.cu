@@ -322,7 +322,6 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.k = k;
         a.sort_queries = !(flags & KD_NO_SORT);
         a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
-        a.warp_served = (flags & KD_WARP_SERVED) != 0;
         DevBuf bq, br, be, bd, bi, bc, bctr;
         if (dev_ptrs) {
             a.queries = queries; a.radii = radii; a.excl = exclude_ids;

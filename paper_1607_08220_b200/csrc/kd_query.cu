@@ -508,295 +508,6 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     }
 }
 
-// ----------------------------------------------------------------------------
-// Warp-served leaves (KD_WARP_SERVED; experimental: serialised serves expose memory latency).  Persistent warps; each lane owns one query at a
-// time (fetched dynamically from the leaf-sorted order) and walks the tree on
-// its own: descend with near-child-first, pushing admissible far children.
-// Leaf buckets are not scanned lane-by-lane: the warp serves the pending
-// leaves one at a time -- lane j evaluates bucket point j against the owning
-// lane's query (a 32-point bucket is one step instead of 32), candidates that
-// can still enter are found with a ballot and inserted by the owner.  The
-// owner re-checks every candidate against its current state, so the result is
-// exactly the sequential (sq_dist, id) top-k.  For float trees an fp32 filter
-// (make_thr: rigorous bound, no candidate can be lost) skips the binary64
-// evaluation of points that cannot enter.
-// ----------------------------------------------------------------------------
-template <typename T, int DT, int KM>
-__global__ void __launch_bounds__(128)
-k_knn_warp(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
-           const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
-           const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
-           const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
-           int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
-    constexpr int DC = Dims<DT>::cap;
-    constexpr int POOL = 64;
-    constexpr bool F32 = sizeof(T) == 4;
-    const int D = DT > 0 ? DT : dims_rt;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1;
-
-    double q[DC];
-    float q32[DC];
-    double radius = 0.0, qnorm = 0.0;
-    uint64_t ex = ~0ULL;
-    const bool has_ex = excl != nullptr;
-    int64_t qi = -1;
-    int64_t c0 = 0, c1 = 0, c2 = 0;
-    double bd[KM];
-    uint64_t bi[KM];
-    int cnt = 0;
-    double kth_d = 0.0;
-    uint64_t kth_i = 0;
-    float thr32 = INFINITY;
-    float off[DC];
-    int st_node[QCAP];
-    float st_off[QCAP][DC];
-    int sp = 0;
-    int node = -1;
-    long long pool_base = 0;
-    int pool_left = 0;
-    bool exhausted = false;
-
-    auto admissible = [&](float b) {
-        const double bb = (double)b;
-        return cnt < k ? bb < radius : bb <= kth_d;
-    };
-    // fp32 filter threshold: a point whose binary64 distance d can still be
-    // admitted (d <= R) has d32 = sum (c - fl32(q))^2 <= thr(R); with u = 2^-24
-    // and x = R(1+2^-50):  thr = (x + 2u^2|q|^2 + 2u|q| sqrt(x + u^2|q|^2))
-    //                             * (1 + (D+2)u) / (1-2u)^2 * (1 + 2^-40)
-    // (per coordinate |t' - t| <= u|q_d| + u|t'|; fp32 accumulation <= (D+1)u).
-    auto make_thr = [&](double R) {
-        if (!(R < 1e300)) return INFINITY;
-        const double u = 5.9604644775390625e-08;
-        const double x = R * (1.0 + 1e-15);
-        const double uq = u * qnorm;
-        const double tt = (x + 2.0 * uq * uq + 2.0 * uq * sqrt(x + uq * uq)) * (1.0 + (D + 2) * u) /
-                          ((1.0 - 2.0 * u) * (1.0 - 2.0 * u)) * (1.0 + 1e-12);
-        return tt >= 3.0e38 ? INFINITY : __double2float_ru(tt);
-    };
-
-    for (;;) {
-        // ---- hand out queries to idle lanes (warp-local pool refilled 64 at a time)
-        const bool need = node < 0;
-        const unsigned mneed = __ballot_sync(FULL, need);
-        if (mneed && !exhausted) {
-            const int want = __popc(mneed);
-            const int rank = __popc(mneed & lt_mask);
-            long long myq = -1;
-            if (rank < pool_left) myq = pool_base + rank;
-            const int taken = min(want, pool_left);
-            pool_base += taken;
-            pool_left -= taken;
-            if (want > taken) {
-                long long nb = 0;
-                if (lane == 0) nb = (long long)atomicAdd(counter, (unsigned long long)POOL);
-                nb = __shfl_sync(FULL, nb, 0);
-                if (nb >= nq) {
-                    exhausted = true;
-                } else {
-                    pool_base = nb;
-                    pool_left = (int)min((long long)POOL, nq - nb);
-                    const int r2 = rank - taken;
-                    if (need && r2 >= 0 && r2 < pool_left) myq = pool_base + r2;
-                    const int t2 = min(want - taken, pool_left);
-                    pool_base += t2;
-                    pool_left -= t2;
-                }
-            }
-            if (need && myq >= 0 && myq < nq) {
-                qi = order ? (int64_t)order[myq] : myq;
-                double qq = 0.0;
-#pragma unroll
-                for (int d = 0; d < DC; d++) {
-                    q[d] = d < D ? queries[qi * D + d] : 0.0;
-                    q32[d] = __double2float_rn(q[d]);
-                    qq += q[d] * q[d];
-                }
-                qnorm = sqrt(qq) * (1.0 + 1e-12);
-                radius = radii ? radii[qi] : INFINITY;
-                ex = has_ex ? excl[qi] : ~0ULL;
-                cnt = 0;
-                kth_d = radius;
-                kth_i = 0;
-                if constexpr (F32) thr32 = make_thr(radius);
-                c0 = c1 = c2 = 0;
-                sp = 0;
-#pragma unroll
-                for (int d = 0; d < DC; d++) off[d] = 0.0f;
-                node = n_nodes > 0 ? 0 : -2;
-            }
-        }
-        if (node == -2) {  // empty tree
-            out_c[qi] = 0;
-            if (out_ctr) { out_ctr[qi * 3] = 0; out_ctr[qi * 3 + 1] = 0; out_ctr[qi * 3 + 2] = 0; }
-            node = -1;
-        }
-        if (__ballot_sync(FULL, node >= 0) == 0) {
-            if (exhausted) break;
-            continue;
-        }
-        // ---- descend to a leaf
-        int lstart = 0, llen = 0;
-        if (node >= 0) {
-            for (;;) {
-                c0++;
-                const KdNode rec = nodes[node];
-                if (rec.db < 0) {
-                    lstart = rec.a;
-                    llen = -1 - rec.db;
-                    break;
-                }
-                const int dim = rec.db;
-                double qd = q[0];
-#pragma unroll
-                for (int d = 1; d < DC; d++)
-                    if (d == dim) qd = q[d];
-                const bool goleft = qd < rec.v;
-                const int near = goleft ? node + 1 : rec.a;
-                const int far = goleft ? rec.a : node + 1;
-                const float ad = __double2float_rz(fabs(qd - rec.v));
-                float fo[DC];
-                float fb = 0.0f;
-#pragma unroll
-                for (int d = 0; d < DC; d++) {
-                    fo[d] = (d == dim) ? ad : off[d];
-                    if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
-                }
-                if (admissible(fb) && sp < QCAP) {
-                    st_node[sp] = far;
-#pragma unroll
-                    for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
-                    sp++;
-                }
-                node = near;
-            }
-            c1++;
-            c2 += llen;
-        }
-        // ---- serve every pending leaf with the whole warp
-        unsigned pending = __ballot_sync(FULL, node >= 0);
-        while (pending) {
-            const int Q = __ffs(pending) - 1;
-            pending &= pending - 1;
-            const int ls = __shfl_sync(FULL, lstart, Q);
-            const int ln = __shfl_sync(FULL, llen, Q);
-            double qQ[DC];
-            float qQ32[DC];
-#pragma unroll
-            for (int d = 0; d < DC; d++) {
-                if (d < D) {
-                    qQ[d] = __shfl_sync(FULL, q[d], Q);
-                    qQ32[d] = __shfl_sync(FULL, q32[d], Q);
-                }
-            }
-            for (int base = 0; base < ln; base += 32) {
-                const int j = base + lane;
-                // Q's admission state as of now (Q re-checks exactly on insertion)
-                const int cntQ = __shfl_sync(FULL, cnt, Q);
-                const double kQ = __shfl_sync(FULL, kth_d, Q);
-                const double rQ = __shfl_sync(FULL, radius, Q);
-                const float tQ = __shfl_sync(FULL, thr32, Q);
-                bool cand = false;
-                double dist = 0.0;
-                if (j < ln) {
-                    T cv[DC];
-#pragma unroll
-                    for (int d = 0; d < DC; d++)
-                        if (d < D) cv[d] = coords[(int64_t)d * n + ls + j];
-                    bool pass = true;
-                    if constexpr (F32) {
-                        float d32 = 0.0f;
-#pragma unroll
-                        for (int d = 0; d < DC; d++)
-                            if (d < D) {
-                                const float tt = (float)cv[d] - qQ32[d];
-                                d32 = fmaf(tt, tt, d32);
-                            }
-                        pass = !(d32 > tQ);
-                    }
-                    if (pass) {
-#pragma unroll
-                        for (int d = 0; d < DC; d++)
-                            if (d < D) {
-                                const double df = __dsub_rn((double)cv[d], qQ[d]);
-                                dist = __dadd_rn(dist, __dmul_rn(df, df));
-                            }
-                        cand = cntQ < k ? dist < rQ : dist <= kQ;
-                    }
-                }
-                unsigned cm = __ballot_sync(FULL, cand);
-                while (cm) {
-                    const int cl = __ffs(cm) - 1;
-                    cm &= cm - 1;
-                    const double dd = __shfl_sync(FULL, dist, cl);
-                    if (lane == Q) {
-                        const uint64_t id = ids[ls + base + cl];
-                        bool ok = cnt < k ? dd < radius : lexless(dd, id, kth_d, kth_i);
-                        if (has_ex && id == ex) ok = false;
-                        if (ok) {
-                            const int p = cnt < k ? cnt : k - 1;
-#pragma unroll
-                            for (int jj = 0; jj < KM; jj++)
-                                if (jj == p) { bd[jj] = dd; bi[jj] = id; }
-#pragma unroll
-                            for (int jj = KM - 1; jj >= 1; jj--) {
-                                if (jj <= p && lexless(bd[jj], bi[jj], bd[jj - 1], bi[jj - 1])) {
-                                    const double td = bd[jj]; bd[jj] = bd[jj - 1]; bd[jj - 1] = td;
-                                    const uint64_t ti = bi[jj]; bi[jj] = bi[jj - 1]; bi[jj - 1] = ti;
-                                }
-                            }
-                            if (cnt < k) cnt++;
-                            if (cnt == k) {
-#pragma unroll
-                                for (int jj = 0; jj < KM; jj++)
-                                    if (jj == k - 1) { kth_d = bd[jj]; kth_i = bi[jj]; }
-                                if constexpr (F32) thr32 = make_thr(kth_d);
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        // ---- next admissible far child, or finish the query
-        if (node >= 0) {
-            node = -1;
-            while (sp > 0) {
-                sp--;
-                float po[DC];
-                float pb = 0.0f;
-#pragma unroll
-                for (int d = 0; d < DC; d++) {
-                    po[d] = st_off[sp][d];
-                    if (d < D) pb = __fadd_rz(pb, __fmul_rz(po[d], po[d]));
-                }
-                if (admissible(pb)) {
-                    node = st_node[sp];
-#pragma unroll
-                    for (int d = 0; d < DC; d++) off[d] = po[d];
-                    break;
-                }
-                c0++;
-            }
-            if (node < 0) {
-                out_c[qi] = cnt;
-#pragma unroll
-                for (int jj = 0; jj < KM; jj++) {
-                    if (jj < cnt) {
-                        out_d[qi * (int64_t)k + jj] = bd[jj];
-                        out_i[qi * (int64_t)k + jj] = bi[jj];
-                    }
-                }
-                if (out_ctr) {
-                    out_ctr[qi * 3 + 0] = c0;
-                    out_ctr[qi * 3 + 1] = c1;
-                    out_ctr[qi * 3 + 2] = c2;
-                }
-            }
-        }
-    }
-}
-
 // leaf reached by descending with the tie rule (coord >= value goes right);
 // used as the sort key that makes each warp's 32 queries spatially coherent
 template <int DT>
@@ -827,21 +538,15 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             int dev = 0, sms = 148, per_sm = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (!a.warp_served) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_persist<T, DT, KM>, threads, 0);
-            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_warp<T, DT, KM>, threads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_persist<T, DT, KM>, threads, 0);
             const long long want = (a.nq + threads - 1) / threads;
             const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
             unsigned long long* ctr = nullptr;
             KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
             KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-            if (!a.warp_served)
-                k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
-                    t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
-                    (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
-            else
-                k_knn_warp<T, DT, KM><<<grid, threads, 0, st>>>(
-                    t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
-                    (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
+            k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
+                t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
+                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
             cudaFreeAsync(ctr, st);
             return;
         }

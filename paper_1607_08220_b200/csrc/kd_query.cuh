@@ -20,8 +20,7 @@ struct KnnArgs {
     double* heap_d = nullptr;         // [nq][k] scratch when k > 32
     uint64_t* heap_i = nullptr;
     bool sort_queries = true;
-    bool thread_per_query = false;
-    bool warp_served = false;       // experimental warp-served leaf kernel instead of k_knn_persist  // legacy one-thread-per-query traversal (k > 32 always uses it)
+    bool thread_per_query = false;  // one-thread-per-query traversal (k > 32 always uses it)
 };
 
 constexpr int KNN_MAX_DEPTH = 61;  // traversal stack capacity - 3

@@ -28,7 +28,7 @@ ps = core.PointSet.from_rows(rows)
 t = lt.build_local_tree(ps, lt.BuildConfig())
 q = rows[:3000]
 bd, bi, bc = O.brute_knn(ps.coords, ps.ids, q, 6)
-for name, fl in (("persistent", 0), ("warp-served", N.KD_WARP_SERVED), ("thread", N.KD_THREAD_PER_QUERY), ("nosort", N.KD_NO_SORT)):
+for name, fl in (("persistent", 0), ("thread", N.KD_THREAD_PER_QUERY), ("nosort", N.KD_NO_SORT)):
     d, i, c, ctr = lq.find_knn_batch(t, q, 6, flags=fl)
     bad = np.nonzero((d != bd).any(1) | (i != bi).any(1))[0]
     print(name, "mismatching queries:", len(bad), "of", len(q), "ctr mean", ctr.mean(0))
