@@ -262,14 +262,17 @@ __global__ void __launch_bounds__(TILE_THREADS)
 k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
        const T* __restrict__ wb, uint32_t* __restrict__ wf) {
     constexpr int EPT = TILE / TILE_THREADS;
+    constexpr int NW = TILE_THREADS / 32;
     __shared__ T sb[WIN];
     __shared__ uint32_t sf[WIN];
+    __shared__ T q[NW][64];  // per-warp queue of in-window values (keeps the searches warp-dense)
     __shared__ unsigned long long sL;
     const uint32_t t = blockIdx.x;
     const int ni = tile_node(nodes, K, t);
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     const int nw = sp.whi - sp.wlo;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
     const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
     const T* row = src + (int64_t)sp.dim * c.N + nd.start;
@@ -287,24 +290,37 @@ k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx
     if (threadIdx.x == 0) sL = 0;
     __syncthreads();
     const T lo_b = sb[0], hi_b = sb[nw - 1];
-    unsigned long long lc = 0;
+    auto search = [&](T x) {  // upper_bound of x in sb[1 .. nw-1)
+        int lo = 1, len = nw - 2;
+        while (len > 0) {
+            const int half = len >> 1;
+            if (sb[lo + half] <= x) { lo += half + 1; len -= half + 1; } else { len = half; }
+        }
+        atomicAdd(&sf[lo], 1u);
+    };
+    uint32_t lc = 0;
+    int qn = 0;  // warp-uniform queue length
 #pragma unroll
     for (int j = 0; j < EPT; j++) {
         const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-        if (e >= e1) continue;
-        if (v[j] < lo_b) {
-            lc++;
-        } else if (v[j] < hi_b) {
-            int lo = 1, hi = nw - 1;  // upper_bound over the window
-            while (lo < hi) {
-                const int md = (lo + hi) >> 1;
-                if (sb[md] <= v[j]) lo = md + 1; else hi = md;
-            }
-            atomicAdd(&sf[lo], 1u);
+        const bool ok = e < e1;
+        const bool below = ok && v[j] < lo_b;
+        const bool inwin = ok && !below && v[j] < hi_b;
+        lc += below;
+        const unsigned m = __ballot_sync(FULL, inwin);
+        if (inwin) q[warp][qn + __popc(m & ((1u << lane) - 1))] = v[j];
+        qn += __popc(m);
+        if (qn >= 32) {  // one dense round of 32 searches
+            __syncwarp();
+            search(q[warp][qn - 32 + lane]);
+            qn -= 32;
+            __syncwarp();
         }
     }
+    __syncwarp();
+    if (lane < qn) search(q[warp][lane]);
     for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
-    if ((threadIdx.x & 31) == 0 && lc) atomicAdd(&sL, lc);
+    if (lane == 0 && lc) atomicAdd(&sL, (unsigned long long)lc);
     __syncthreads();
     if (threadIdx.x == 0 && sL) atomicAdd(&split[ni].L, sL);
     for (int i = threadIdx.x + 1; i < nw; i += blockDim.x)
@@ -816,6 +832,9 @@ __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, in
                                             typename KeyOf<T>::type& ks, int& lt, int& eq,
                                             typename KeyOf<T>::type& nxt) {
     typedef typename KeyOf<T>::type Key;
+    __builtin_assume(__isShared(row));
+    __builtin_assume(__isShared(pm));
+    __builtin_assume(__isShared(hist));
     const int lane = threadIdx.x & 31;
     constexpr int KB = sizeof(Key) * 8;
     Key prefix = 0;
@@ -892,6 +911,9 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
                           const DevCtx& c, uint32_t* hist, uint32_t* fyslots, int* fylocks, int& out_dim,
                           double& out_val, int& out_nl) {
     typedef typename KeyOf<T>::type Key;
+    __builtin_assume(__isShared(cs));
+    __builtin_assume(__isShared(pm));
+    __builtin_assume(__isShared(hist));
     constexpr int DC = DT > 0 ? DT : 16;
     const int D = DT > 0 ? DT : dims_rt;
     const int lane = threadIdx.x & 31;
@@ -1056,8 +1078,8 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         maxd = max(maxd, rd);
         int dim = -1, nl = 0;
         double val = 0.0;
-        if (nn > c.bucket) sub_split<T, DT>(cs, perm[rd & 1] + st, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val,
-                                            nl);
+        if (nn > c.bucket) sub_split<T, DT>(cs, ((rd & 1) ? perm[1] : perm[0]) + st, nn, ts, D, path, c, hist, fyslots,
+                                            fylocks, dim, val, nl);
         if (dim < 0) {
             if (lane == 0) {
                 out_nodes[pre] = KdNode{0.0, (int32_t)(tk.start + st), -1 - nn};
