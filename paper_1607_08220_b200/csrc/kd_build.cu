@@ -27,6 +27,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "kd_common.cuh"
@@ -105,7 +106,7 @@ __device__ __forceinline__ double ssd_bound(double s2, double sabs, int t) {
 // ============================================================================
 // k_sample: one warp per breadth-first node
 // ============================================================================
-template <typename T, int DT>
+template <typename T, int DT, bool BIG>
 __global__ void __launch_bounds__(SAMPLE_WARPS * 32)
 k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
          T* __restrict__ wb, uint32_t* __restrict__ wf) {
@@ -114,18 +115,21 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ni = blockIdx.x * SAMPLE_WARPS + warp;
     if (ni >= K) return;
-    uint64_t* skeys = reinterpret_cast<uint64_t*>(smem_raw) + warp * MAXS;
-    uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * 8) + warp * MAXS;
     const LNode nd = nodes[ni];
     const uint32_t n = (uint32_t)nd.n;
+    // nodes above 2^22 points need 64-bit (target, step) keys; they are few and
+    // get their own instantiation so the common one stays small
+    if (BIG != (n > (1u << 22))) return;
+    typedef typename std::conditional<BIG, uint64_t, uint32_t>::type FK;
+    FK* skeys = reinterpret_cast<FK*>(smem_raw) + warp * MAXS;
+    uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * sizeof(FK)) + warp * MAXS;
     const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
 
     // --- variance sample (local_tree.py:122-132)
     const int take = (int)min((int64_t)n, c.vs);
     const uint64_t vseed = node_seed(c.seed, nd.path, 0);
-    if (n <= (1u << 22)) fy_resolve<32, uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(skeys), picked);
-    else fy_resolve<32, uint64_t>(n, take, vseed, skeys, picked);
+    fy_resolve<32, FK>(n, take, vseed, skeys, picked);
 
     int d0 = 0;
     double b0 = 0.0, e0 = 0.0;
@@ -187,8 +191,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const int m = (int)min((int64_t)n, c.ms);
     const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
     __syncwarp();
-    if (n <= (1u << 22)) fy_resolve<32, uint32_t>(n, m, mseed, reinterpret_cast<uint32_t*>(skeys), picked);
-    else fy_resolve<32, uint64_t>(n, m, mseed, skeys, picked);
+    fy_resolve<32, FK>(n, m, mseed, skeys, picked);
     typedef typename KeyOf<T>::type Key;
     const T* row = src + (int64_t)d0 * N + nd.start;
     Key kv[32];
@@ -755,7 +758,7 @@ struct TopStore {
 
 __global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* __restrict__ split, DevCtx c,
                            int dst_parity, int src_parity, int child_base, TopStore ts, LNode* next,
-                           unsigned long long* next_ctr, Task* tasks, int* task_ctr) {
+                           unsigned long long* next_ctr, Task* tasks, int* task_ctr, int* next_max) {
     const int ni = blockIdx.x * blockDim.x + threadIdx.x;
     if (ni >= K) return;
     const LNode nd = nodes[ni];
@@ -787,6 +790,7 @@ __global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* 
             const int idx = (int)(old >> 32);
             next[idx] = LNode{cs[k], cn[k], nd.depth + 1, cp[k], slot[k], (uint32_t)(old & 0xFFFFFFFFULL)};
             ts.kind[slot[k]] = TS_INTERIOR;
+            atomicMax(next_max, cn[k]);
         } else {
             const int t = atomicAdd(task_ctr, 1);
             tasks[t] = Task{cs[k], cn[k], nd.depth + 1, cp[k], slot[k], dst_parity, 0, 0};
@@ -928,16 +932,19 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
         eb[d] = 0.0;
         if (d >= D) continue;
         const T* row = cs + d * ts;
+        // one pass: shifted sums y = x - x0 (x0 = node's first value); S2 = sum y^2 - (sum y)^2 / n
+        const double x0 = (double)row[pm[0]];
         Key kmn = ~(Key)0, kmx = 0;
-        double s1 = 0.0, sa = 0.0;
+        double s1 = 0.0, sq = 0.0;
 #pragma unroll 4
         for (int i = lane; i < n; i += 32) {
             const T v = row[pm[i]];
             const Key k = tkey(v);
             kmn = k < kmn ? k : kmn;
             kmx = k > kmx ? k : kmx;
-            s1 = __dadd_rn(s1, (double)v);
-            sa = __dadd_rn(sa, fabs((double)v));
+            const double y = __dsub_rn((double)v, x0);
+            s1 = __dadd_rn(s1, y);
+            sq = __dadd_rn(sq, __dmul_rn(y, y));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -948,16 +955,12 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
         if (kmn == kmx) continue;
         ncmask |= 1u << d;
         s1 = warp_sum(s1);
-        sa = warp_sum(sa);
-        const double mean = __ddiv_rn(s1, (double)n);
-        double s2 = 0.0;
-#pragma unroll 4
-        for (int i = lane; i < n; i += 32) {
-            const double df = __dsub_rn((double)row[pm[i]], mean);
-            s2 = __dadd_rn(s2, __dmul_rn(df, df));
-        }
-        s2v[d] = warp_sum(s2);
-        eb[d] = ssd_bound(s2v[d], sa, n);
+        sq = warp_sum(sq);
+        const double bb = __dmul_rn(s1, s1) / (double)n;
+        s2v[d] = sq - bb;
+        // rigorous bound on |computed - reference two-pass value| (both vs the exact sum of
+        // squared deviations): shifted-sum rounding + the reference's own two-pass error
+        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq + bb) + 1e-300;
         if (best < 0 || s2v[d] > bs) { best = d; bs = s2v[d]; be = eb[d]; }
     }
     out_dim = -1;
@@ -1218,7 +1221,7 @@ static void dfree(void* p, cudaStream_t st) {
 // persistent pinned words for the per-level counter read-back (page-locking per build costs ms)
 // (one per host thread: concurrent builds from several rank threads must not share it)
 static unsigned long long* pinned_counters(int) {
-    static thread_local unsigned long long* p = nullptr;
+    static thread_local unsigned long long* p = nullptr;  // [0] next level, [1] tasks|slow, [2] max node
     if (!p) KD_CUDA(cudaMallocHost(&p, 4 * sizeof(unsigned long long)));
     return p;
 }
@@ -1325,7 +1328,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     Task* tasks = dalloc<Task>(task_cap, st);
     int* task_ctr = dalloc<int>(1, st);
     KD_CUDA(cudaMemsetAsync(task_ctr, 0, sizeof(int), st));
-    unsigned long long* next_ctr = dalloc<unsigned long long>(1, st);
+    unsigned long long* next_ctr = dalloc<unsigned long long>(2, st);  // [0] packed count/tiles, [1] max child size
     int* slow_count = dalloc<int>(1, st);
     unsigned long long* h_ctr = nullptr;
     h_ctr = pinned_counters(out->device);
@@ -1359,13 +1362,18 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int ntasks_known = K == 0 ? 1 : 0;
     {
     }
-    size_t sample_smem = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
-    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
-    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem));
+    const size_t sample_smem32 = (size_t)SAMPLE_WARPS * MAXS * (4 + 4);
+    const size_t sample_smem64 = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));
+    KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
+    int64_t max_node = n;  // largest node of the current level (read back with the level counters)
     while (K > 0) {
         LNode* lv = levels.back();
+        const bool big_levels = max_node > (int64_t(1) << 22);
         // capacity: children slots and tasks
         if (ts_used + 2 * (size_t)K + 1 > ts_cap) {
             size_t nc = std::max(ts_cap * 2, ts_used + 2 * (size_t)K + 1);
@@ -1393,12 +1401,16 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         uint32_t* tile_left = dalloc<uint32_t>(tiles + 1, st);
         uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
         KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
-        if (dims == 3)
-            k_sample<T, 3><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
-                buf[par], lv, K, c, split, wb, wf);
-        else
-            k_sample<T, 0><<<(K + SAMPLE_WARPS - 1) / SAMPLE_WARPS, SAMPLE_WARPS * 32, sample_smem, st>>>(
-                buf[par], lv, K, c, split, wb, wf);
+        {
+            const unsigned sg = (unsigned)((K + SAMPLE_WARPS - 1) / SAMPLE_WARPS);
+            if (dims == 3) {
+                k_sample<T, 3, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(buf[par], lv, K, c, split, wb, wf);
+                if (big_levels) k_sample<T, 3, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(buf[par], lv, K, c, split, wb, wf);
+            } else {
+                k_sample<T, 0, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(buf[par], lv, K, c, split, wb, wf);
+                if (big_levels) k_sample<T, 0, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(buf[par], lv, K, c, split, wb, wf);
+            }
+        }
         k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, wb, wf);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(buf[par], lv, c, split, slow_list, slow_count);
@@ -1419,14 +1431,15 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         }
 #undef KD_SCATTER
         LNode* next = dalloc<LNode>(2 * (size_t)K, st);
-        KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long), st));
+        KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long) + sizeof(int), st));
         k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, par, (int)ts_used, ts, next, next_ctr,
-                                                    tasks, task_ctr);
+                                                    tasks, task_ctr, reinterpret_cast<int*>(next_ctr + 1));
         KD_CUDA(cudaGetLastError());
         KD_CUDA(cudaMemcpyAsync(&h_ctr[0], next_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         KD_CUDA(cudaMemcpyAsync(&h_ctr[1], task_ctr, sizeof(int), cudaMemcpyDeviceToHost, st));
         int* h_slow = reinterpret_cast<int*>(&h_ctr[1]) + 1;
         KD_CUDA(cudaMemcpyAsync(h_slow, slow_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KD_CUDA(cudaMemcpyAsync(&h_ctr[2], next_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         KD_CUDA(cudaStreamSynchronize(st));
         tr.mark("level done", (int)levels.size());
         slow_total += *h_slow;
@@ -1437,6 +1450,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         ts_used += 2 * (size_t)K;
         K = (int)(h_ctr[0] >> 32);
         tiles = (uint32_t)(h_ctr[0] & 0xFFFFFFFFULL);
+        max_node = (int64_t)(int32_t)(h_ctr[2] & 0xFFFFFFFFULL);
         par = 1 - par;
         if (K > 0) levels.push_back(next);
         else dfree(next, st);

@@ -156,3 +156,120 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
 }
 
 }  // namespace kdb
+
+namespace kdb {
+
+// ---------------------------------------------------------------------------
+// fy_hash: the same partial Fisher-Yates draw as fy_resolve, resolved with a
+// shared-memory hash table (target slot -> list of steps that targeted it)
+// instead of a sort.  For step j, pred(j) = latest earlier step with the same
+// target; V(t) = value at slot t before step t follows the latest step < t that
+// targeted t.  Lists are unordered; "latest earlier" is a max over the list.
+//   hkey/hhead: FY_HS words each, hnext: m words, out: m words.
+// ---------------------------------------------------------------------------
+constexpr int FY_HS = 2048;
+constexpr uint32_t FY_EMPTY = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t fy_slot0(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 11); }
+
+__device__ __forceinline__ int fy_find(const uint32_t* hkey, uint32_t t) {
+    uint32_t s = fy_slot0(t);
+    for (;;) {
+        const uint32_t k = hkey[s];
+        if (k == t) return (int)s;
+        if (k == FY_EMPTY) return -1;
+        s = (s + 1) & (FY_HS - 1);
+    }
+}
+
+// latest step < before in the list of slot s (FY_EMPTY if none)
+__device__ __forceinline__ uint32_t fy_latest(const uint32_t* hhead, const uint32_t* hnext, int s, uint32_t before) {
+    uint32_t best = FY_EMPTY;
+    for (uint32_t x = hhead[s]; x != FY_EMPTY; x = hnext[x])
+        if (x < before && (best == FY_EMPTY || x > best)) best = x;
+    return best;
+}
+
+__device__ __forceinline__ void fy_hash(uint32_t n, int m, uint64_t seed, uint32_t* hkey, uint32_t* hhead, uint32_t* hnext,
+                        uint32_t* out) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < FY_HS; i += 32) { hkey[i] = FY_EMPTY; hhead[i] = FY_EMPTY; }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) {
+        const uint64_t z = rng_at(seed, (uint64_t)j);
+        const uint32_t t = (uint32_t)j + (uint32_t)mod_u64_u32(z, n - (uint32_t)j);
+        uint32_t s = fy_slot0(t);
+        for (;;) {
+            const uint32_t old = atomicCAS(&hkey[s], FY_EMPTY, t);
+            if (old == FY_EMPTY || old == t) break;
+            s = (s + 1) & (FY_HS - 1);
+        }
+        hnext[j] = atomicExch(&hhead[s], (uint32_t)j);
+        out[j] = t;
+    }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) {
+        const uint32_t t = out[j];
+        uint32_t cur = fy_latest(hhead, hnext, fy_find(hkey, t), (uint32_t)j);
+        uint32_t val = t;
+        if (cur != FY_EMPTY) {
+            for (;;) {  // V(cur): value at slot cur before step cur
+                const int s2 = fy_find(hkey, cur);
+                const uint32_t p = s2 < 0 ? FY_EMPTY : fy_latest(hhead, hnext, s2, cur);
+                if (p == FY_EMPTY) { val = cur; break; }
+                cur = p;
+            }
+        }
+        out[j] = val;
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// warp_radix_sort: stable LSD radix sort (8-bit digits) of m keys held in
+// shared memory (a -> sorted in a; b is scratch of m keys; cnt is 256 words).
+// Within a 32-key chunk, equal digits keep lane order via __match_any_sync.
+// ---------------------------------------------------------------------------
+template <typename K>
+__device__ void warp_radix_sort(K* a, K* b, int m, uint32_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    constexpr int KB = sizeof(K) * 8;
+    for (int shift = 0; shift < KB; shift += 8) {
+        for (int i = lane; i < 256; i += 32) cnt[i] = 0;
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) atomicAdd(&cnt[(int)((a[i] >> shift) & 255)], 1u);
+        __syncwarp();
+        // exclusive scan of the 256 counters (8 per lane)
+        uint32_t h[8], s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) { h[j] = cnt[lane * 8 + j]; s += h[j]; }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - s;
+#pragma unroll
+        for (int j = 0; j < 8; j++) { cnt[lane * 8 + j] = run; run += h[j]; }
+        __syncwarp();
+        for (int c = 0; c < m; c += 32) {
+            const int i = c + lane;
+            const bool v = i < m;
+            const K key = v ? a[i] : (K)0;
+            const uint32_t dg = v ? (uint32_t)((key >> shift) & 255) : 256u + lane;
+            const unsigned peers = __match_any_sync(FULL, dg);
+            const int r = __popc(peers & ((1u << lane) - 1));
+            const uint32_t base = v ? cnt[dg] : 0;
+            __syncwarp();
+            if (v) b[base + r] = key;
+            if (v && r == 0) cnt[dg] = base + __popc(peers);
+            __syncwarp();
+        }
+        { K* t = a; a = b; b = t; }  // result now in `a` (pointer swap)
+        __syncwarp();
+    }
+    // KB/8 passes: an even number for 32- and 64-bit keys, so the data ends in the caller's `a`
+}
+
+}  // namespace kdb
