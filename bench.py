@@ -45,8 +45,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
-    p.add_argument("--n", type=int, default=None, help="override point count (debug)")
-    p.add_argument("--q", type=int, default=None, help="override query count (debug)")
+    p.add_argument("--points", dest="n", type=int, default=None, help="override points per GPU (debug)")
+    p.add_argument("--queries", dest="q", type=int, default=None, help="override queries per GPU (debug)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-build-sample", type=int, default=4_000_000)
@@ -134,7 +134,8 @@ def cpu_baseline_leg(cfgname, w, tree, sel_queries, args, seed=0):
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     nb = min(args.cpu_build_sample, w.n)
-    rows = __import__("paper_1607_08220_b200.workloads", fromlist=["x"]).make_points_numpy(cfgname, nb, seed=77)
+    from paper_1607_08220_b200.workloads import make_points
+    rows = make_points(cfgname, "cuda", seed=77, n=nb).cpu().numpy()  # same law, bounded sample
     coords = np.ascontiguousarray(rows.T.astype(np.float64))
     O.build_tree(coords[:, :100_000], bucket_size=w.leaf, seed=seed, threads=cores)  # warm
     t0 = time.perf_counter()
@@ -168,7 +169,11 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     nb = min(args.cpu_build_sample, w.n)
     nqs = min(args.cpu_query_sample, w.q)
-    rows = make_points_numpy(args.config, nb, seed=77)
+    try:
+        rows = make_points_numpy(args.config, nb, seed=77)
+    except ValueError:
+        from paper_1607_08220_b200.workloads import make_points
+        rows = make_points(args.config, "cpu", seed=77, n=nb).numpy()
     coords = np.ascontiguousarray(rows.T.astype(np.float64))
     rng = np.random.default_rng(5)
     sel = rng.choice(nb, size=min(nqs, nb), replace=False)
@@ -333,7 +338,7 @@ def run_b200(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        nqs = min(args.cpu_query_sample, q)
+        nqs = min(args.cpu_query_sample if w.dims <= 3 else 2000, q)  # 10-D queries scan ~1e5 points each
         qsel = queries[:nqs].cpu().numpy()
         cpu = cpu_baseline_leg(args.config, w, tree, qsel, args)
 
@@ -385,10 +390,126 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_b200_multi(args):
+    """N > 1 (torchrun, one process per GPU): the PANDA global tier on NCCL.
+    Weak scaling: every rank owns 64M points / 16M queries of the workload law;
+    a step = global planes (sample all-gather + summed device histograms) +
+    all-to-all redistribution + local build, then the 5-step distributed query
+    (route, local KNN, r' forwarding, radius KNN, merge) -- all device-resident."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, rank_build_global
+    from paper_1607_08220_b200.comm import TorchComm
+    from paper_1607_08220_b200.dist_device import DeviceRegions, rank_query_device
+    from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
+    from paper_1607_08220_b200.workloads import CONFIGS, make_points, make_queries
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = TorchComm()
+    w = CONFIGS[args.config]
+    n = args.n or w.n
+    q = args.q or w.q
+    rows = make_points(args.config, dev, seed=1000 + rank, n=n)
+    coords = rows.t().contiguous()
+    ids = torch.arange(n, dtype=torch.int64, device=dev) + rank * n
+    queries, sel = make_queries(args.config, rows, dev, seed=2000 + rank, q=q)
+    excl = (sel + rank * n) if sel is not None else None
+    qids = torch.arange(q, dtype=torch.int64, device=dev)
+    ccfg, bcfg = ClusterConfig(seed=0), BuildConfig(bucket_size=w.leaf, seed=0)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        gt, pts, st = rank_build_global(comm, DevicePoints(coords, ids), ccfg)
+        tree = build_local_tree_device(pts.coords, pts.ids, bcfg)
+        e[1].record(stream)
+        stats = {}
+        out = rank_query_device(comm, tree, DeviceRegions(gt, dev), qids, queries, w.k, excl=excl, stats=stats)
+        e[2].record(stream)
+        return tree, out, e, st, stats
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(); dist.barrier(); torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    evs, moved, fwd = [], 0, 0
+    for _ in range(args.steps):
+        tree, out, e, st, stats = step()
+        evs.append(e)
+        moved += st["points_moved"]
+        fwd += stats.get("queries_forwarded", 0)
+    torch.cuda.synchronize(); dist.barrier(); torch.cuda.synchronize()
+    clk = clocks.stop()
+    tb = sum(a.elapsed_time(b) for a, b, _ in evs) / len(evs) / 1e3
+    tq = sum(b.elapsed_time(c) for _, b, c in evs) / len(evs) / 1e3
+    t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tb, tq = t.tolist()
+    tot = torch.tensor([moved / args.steps, fwd / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot)
+    # e2e: pinned host inputs -> device -> distributed build + query -> results to host
+    h_c = coords.cpu().pin_memory()
+    h_q = queries.cpu().pin_memory()
+    te = []
+    for it in range(2 + min(args.steps, 2)):
+        torch.cuda.synchronize(); dist.barrier()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dc = h_c.to(dev, non_blocking=True)
+        dq = h_q.to(dev, non_blocking=True)
+        gt, pts, _ = rank_build_global(comm, DevicePoints(dc, ids), ccfg)
+        tr = build_local_tree_device(pts.coords, pts.ids, bcfg)
+        od, oi, oc = rank_query_device(comm, tr, DeviceRegions(gt, dev), qids, dq, w.k, excl=excl)
+        od.cpu(); oi.cpu()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if it >= 2:
+            te.append(a.elapsed_time(b) / 1e3)
+    tt = torch.tensor([float(np.mean(te))], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    te_m = tt.item()
+    if rank == 0:
+        peak, peak_kind = peaks()
+        bbytes, levels_model = build_bytes(n, w.dims, w.leaf)
+        ach_b = bbytes / tb / 1e9
+        line = {
+            "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
+            "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n_per_gpu": n, "q_per_gpu": q, "k": w.k, "leaf": w.leaf,
+                       "dims": w.dims, "parallelism": f"global kd-tree over {world} GPUs (NCCL all-to-all)",
+                       "l2": "inputs larger than L2"},
+            "ms_build": tb * 1e3, "ms_knn": tq * 1e3,
+            "roofline": {"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s", "frac": ach_b / peak,
+                         "traffic": None, "kernel": "per-GPU local build + global tier", "peak_kind": peak_kind,
+                         "model": f"N*L*(8D+12) per GPU, L={levels_model}"},
+            "knn": {"value": world * q / tq, "unit": "queries/s"},
+            "points_moved_per_step": int(tot[0].item()), "queries_forwarded_per_step": int(tot[1].item()),
+            "gpu_launches": None, "clocks": clk,
+            "e2e": {"value": world * n / te_m / 1e6, "unit": "Mpoints/s (build + query, host in/out)",
+                    "h2d_bytes_per_step": int(n * w.dims * 4 + q * w.dims * 8),
+                    "d2h_bytes_per_step": int(q * w.k * 16), "ms_step": te_m * 1e3},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("KDB_FORCE_GLOBAL"):
+        run_b200_multi(args)
     else:
         run_b200(args)
 

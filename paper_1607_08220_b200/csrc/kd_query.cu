@@ -28,8 +28,10 @@
 namespace kdb {
 
 constexpr int QCAP = 64;  // traversal stack capacity (tree depth + 2)
-// the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves (measured 34 vs 44 ms on C2)
-constexpr bool kPersistF32Filter = false;
+// the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
+// (measured 34 vs 44 ms on C2); in higher dimensions the binary64 leaf scan dominates and it pays off
+template <int DT>
+constexpr bool kPersistF32Filter = (DT == 0);
 
 __device__ __forceinline__ bool lexless(double d0, uint64_t i0, double d1, uint64_t i1) {
     return d0 < d1 || (d0 == d1 && i0 < i1);
@@ -359,7 +361,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 kth_d = radius;
                 kth_i = 0;
                 c0 = c1 = c2 = 0;
-                if constexpr (kPersistF32Filter && sizeof(T) == 4) {
+                if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
                     double qq = 0.0;
 #pragma unroll
                     for (int d = 0; d < DC; d++) {
@@ -399,7 +401,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
 #pragma unroll
                     for (int d = 0; d < DC; d++)
                         if (d < D) cv[d] = coords[(int64_t)d * n + i];
-                    if constexpr (kPersistF32Filter && sizeof(T) == 4) {
+                    if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
                         float d32 = 0.0f;
 #pragma unroll
                         for (int d = 0; d < DC; d++) {
@@ -442,7 +444,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
 #pragma unroll
                         for (int j = 0; j < KM; j++)
                             if (j == k - 1) { kth_d = bd[j]; kth_i = bi[j]; }
-                        if constexpr (kPersistF32Filter && sizeof(T) == 4) thr32 = make_thr(kth_d);
+                        if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) thr32 = make_thr(kth_d);
                     }
                 }
                 break;

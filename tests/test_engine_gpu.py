@@ -66,3 +66,43 @@ def test_unsplittable_raises():
     parts = [PointSet.from_rows(rows[:25]), PointSet.from_rows(rows[25:], ids=np.arange(25, 50, dtype=np.uint64))]
     with pytest.raises(UnsplittableDataError):
         build_global_tree(parts, ClusterConfig(seed=0))
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_device_resident_protocol(p, oracle):
+    """dist_device.rank_query_device over in-process ranks (device tensors through
+    the communicator), global tier built with the device kernels."""
+    import torch
+    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, rank_build_global
+    from paper_1607_08220_b200.comm import run_ranks
+    from paper_1607_08220_b200.dist_device import DeviceRegions, rank_query_device
+    from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
+    rows = make_rows(60000, 3, 23, "halo-f32")
+    n = rows.shape[0]
+    qsel = np.random.default_rng(3).choice(n, 3000, replace=False)
+    k = 5
+
+    def prog(comm):
+        dev = comm.device
+        lo, hi = round(comm.rank * n / p), round((comm.rank + 1) * n / p)
+        c = torch.as_tensor(rows[lo:hi].T.astype(np.float32)).to(dev).contiguous()
+        ids = torch.arange(lo, hi, dtype=torch.int64, device=dev)
+        gt, pts, _ = rank_build_global(comm, DevicePoints(c, ids), ClusterConfig(seed=1))
+        tree = build_local_tree_device(pts.coords, pts.ids, BuildConfig(seed=1))
+        mine = qsel[qsel % p == comm.rank]
+        q = torch.as_tensor(rows[mine]).to(dev)
+        ex = torch.as_tensor(mine.astype(np.int64)).to(dev)
+        st = {}
+        d, i, cnt = rank_query_device(comm, tree, DeviceRegions(gt, dev), ex, q, k, excl=ex, stats=st)
+        return mine, d.cpu().numpy(), i.cpu().numpy(), cnt.cpu().numpy(), st
+
+    outs = run_ranks(p, prog, [() for _ in range(p)])
+    coords = np.ascontiguousarray(rows.T)
+    ids = np.arange(n, dtype=np.uint64)
+    for mine, d, i, cnt, st in outs:
+        bd, bi, bc = oracle.brute_knn(coords, ids, rows[mine], k + 1)
+        for r in range(mine.shape[0]):
+            keep = bi[r, :bc[r]] != mine[r]
+            assert np.array_equal(d[r], bd[r, :bc[r]][keep][:k])
+            assert np.array_equal(i[r].view(np.uint64), bi[r, :bc[r]][keep][:k])
+        assert (cnt == k).all()
