@@ -37,6 +37,32 @@ __device__ __forceinline__ bool lexless(double d0, uint64_t i0, double d1, uint6
     return d0 < d1 || (d0 == d1 && i0 < i1);
 }
 
+// insert (d, id) into the ascending list (bd, bi)[0 .. cnt) of capacity k <= KM,
+// dropping the last entry when full (the caller has checked that it enters):
+// one descending pass, each slot either keeps, shifts from its predecessor, or
+// takes the new entry.
+template <int KM>
+__device__ __forceinline__ void topk_insert(double (&bd)[KM], uint64_t (&bi)[KM], int& cnt, int k, double d,
+                                            uint64_t id) {
+    const int last = cnt < k ? cnt : k - 1;  // slot that receives a value
+    bool placed = false;
+#pragma unroll
+    for (int jj = KM - 1; jj >= 0; jj--) {
+        if (jj <= last && !placed) {
+            const bool shift = jj > 0 && lexless(d, id, bd[jj > 0 ? jj - 1 : 0], bi[jj > 0 ? jj - 1 : 0]);
+            if (shift) {
+                bd[jj] = bd[jj > 0 ? jj - 1 : 0];
+                bi[jj] = bi[jj > 0 ? jj - 1 : 0];
+            } else {
+                bd[jj] = d;
+                bi[jj] = id;
+                placed = true;
+            }
+        }
+    }
+    if (cnt < k) cnt++;
+}
+
 template <int DT>
 struct Dims {
     static constexpr int cap = DT > 0 ? DT : 16;
@@ -428,18 +454,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                     const uint64_t id = ids[i];
                     if (has_ex && id == ex) continue;
                     if (cnt == k && !lexless(dist, id, kth_d, kth_i)) continue;
-                    const int p = cnt < k ? cnt : k - 1;
-#pragma unroll
-                    for (int j = 0; j < KM; j++)
-                        if (j == p) { bd[j] = dist; bi[j] = id; }
-#pragma unroll
-                    for (int j = KM - 1; j >= 1; j--) {
-                        if (j <= p && lexless(bd[j], bi[j], bd[j - 1], bi[j - 1])) {
-                            const double td = bd[j]; bd[j] = bd[j - 1]; bd[j - 1] = td;
-                            const uint64_t ti = bi[j]; bi[j] = bi[j - 1]; bi[j - 1] = ti;
-                        }
-                    }
-                    if (cnt < k) cnt++;
+                    topk_insert<KM>(bd, bi, cnt, k, dist, id);
                     if (cnt == k) {
 #pragma unroll
                         for (int j = 0; j < KM; j++)
@@ -561,7 +576,12 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
 template <typename T, int DT>
 static void dispatch_k(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, const uint32_t* home,
                        cudaStream_t st) {
-    if (a.k <= 8) launch_knn<T, DT, 8>(t, a, order, home, st);
+    if (a.k == 1) launch_knn<T, DT, 1>(t, a, order, home, st);
+    else if (a.k == 2) launch_knn<T, DT, 2>(t, a, order, home, st);
+    else if (a.k <= 4) launch_knn<T, DT, 4>(t, a, order, home, st);
+    else if (a.k == 5) launch_knn<T, DT, 5>(t, a, order, home, st);
+    else if (a.k == 6) launch_knn<T, DT, 6>(t, a, order, home, st);
+    else if (a.k <= 8) launch_knn<T, DT, 8>(t, a, order, home, st);
     else if (a.k <= 16) launch_knn<T, DT, 16>(t, a, order, home, st);
     else if (a.k <= 32) launch_knn<T, DT, 32>(t, a, order, home, st);
     else launch_knn<T, DT, 0>(t, a, order, home, st);
