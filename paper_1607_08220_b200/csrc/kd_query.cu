@@ -63,6 +63,36 @@ __device__ __forceinline__ void topk_insert(double (&bd)[KM], uint64_t (&bi)[KM]
     if (cnt < k) cnt++;
 }
 
+// same list keyed by (sq_dist, packed row): ids are only read to break exact
+// distance ties (lexicographic (d, id) order is preserved exactly)
+__device__ __forceinline__ bool lexless_pos(double d0, uint32_t p0, double d1, uint32_t p1,
+                                            const uint64_t* __restrict__ ids) {
+    return d0 < d1 || (d0 == d1 && ids[p0] < ids[p1]);
+}
+
+template <int KM>
+__device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
+                                                uint32_t p, const uint64_t* __restrict__ ids) {
+    const int last = cnt < k ? cnt : k - 1;
+    bool placed = false;
+#pragma unroll
+    for (int jj = KM - 1; jj >= 0; jj--) {
+        if (jj <= last && !placed) {
+            const int pj = jj > 0 ? jj - 1 : 0;
+            const bool shift = jj > 0 && lexless_pos(d, p, bd[pj], bp[pj], ids);
+            if (shift) {
+                bd[jj] = bd[pj];
+                bp[jj] = bp[pj];
+            } else {
+                bd[jj] = d;
+                bp[jj] = p;
+                placed = true;
+            }
+        }
+    }
+    if (cnt < k) cnt++;
+}
+
 template <int DT>
 struct Dims {
     static constexpr int cap = DT > 0 ? DT : 16;
@@ -309,10 +339,10 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     int64_t qi = -1;
     int64_t c0 = 0, c1 = 0, c2 = 0;
     double bd[KM];
-    uint64_t bi[KM];
+    uint32_t bp[KM];  // packed rows; ids[bp] at output
     int cnt = 0;
     double kth_d = 0.0;
-    uint64_t kth_i = 0;
+    uint32_t kth_p = 0;
     float off[DC];
     int st_node[QCAP];
     float st_off[QCAP][DC];
@@ -385,7 +415,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 ex = has_ex ? excl[qi] : ~0ULL;
                 cnt = 0;
                 kth_d = radius;
-                kth_i = 0;
+                kth_p = 0;
                 c0 = c1 = c2 = 0;
                 if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
                     double qq = 0.0;
@@ -451,14 +481,13 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                     } else if (!(dist <= kth_d)) {
                         continue;
                     }
-                    const uint64_t id = ids[i];
-                    if (has_ex && id == ex) continue;
-                    if (cnt == k && !lexless(dist, id, kth_d, kth_i)) continue;
-                    topk_insert<KM>(bd, bi, cnt, k, dist, id);
+                    if (has_ex && ids[i] == ex) continue;
+                    if (cnt == k && !lexless_pos(dist, (uint32_t)i, kth_d, kth_p, ids)) continue;
+                    topk_insert_pos<KM>(bd, bp, cnt, k, dist, (uint32_t)i, ids);
                     if (cnt == k) {
 #pragma unroll
                         for (int j = 0; j < KM; j++)
-                            if (j == k - 1) { kth_d = bd[j]; kth_i = bi[j]; }
+                            if (j == k - 1) { kth_d = bd[j]; kth_p = bp[j]; }
                         if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) thr32 = make_thr(kth_d);
                     }
                 }
@@ -513,7 +542,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
             for (int j = 0; j < KM; j++) {
                 if (j < cnt) {
                     out_d[qi * (int64_t)k + j] = bd[j];
-                    out_i[qi * (int64_t)k + j] = bi[j];
+                    out_i[qi * (int64_t)k + j] = ids[bp[j]];
                 }
             }
             if (out_ctr) {
