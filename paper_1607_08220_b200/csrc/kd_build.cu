@@ -833,6 +833,7 @@ __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
 // select with a per-warp shared-memory histogram.
 template <typename T>
 __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, int n, int kth, uint32_t* hist,
+                                            typename KeyOf<T>::type kmin_, typename KeyOf<T>::type kmax_,
                                             typename KeyOf<T>::type& ks, int& lt, int& eq,
                                             typename KeyOf<T>::type& nxt) {
     typedef typename KeyOf<T>::type Key;
@@ -841,10 +842,15 @@ __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, in
     __builtin_assume(__isShared(hist));
     const int lane = threadIdx.x & 31;
     constexpr int KB = sizeof(Key) * 8;
-    Key prefix = 0;
+    // every key lies in [kmin_, kmax_]: their common high bytes need no pass
+    const Key diff = kmin_ ^ kmax_;
+    int top = KB - 1;
+    while (top > 0 && !((diff >> top) & 1)) top--;
+    const int start = (top / 8) * 8;
+    Key prefix = start + 8 >= KB ? (Key)0 : (kmin_ & ((~(Key)0) << (start + 8)));
     int rem = kth;
 #pragma unroll 1
-    for (int shift = KB - 8; shift >= 0; shift -= 8) {
+    for (int shift = start; shift >= 0; shift -= 8) {
         for (int i = lane; i < 256; i += 32) hist[i] = 0;
         __syncwarp();
         const Key hmask = shift + 8 >= KB ? (Key)0 : (~(Key)0) << (shift + 8);
@@ -925,6 +931,7 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     int best = -1;
     double bs = 0.0, be = 0.0;
     double s2v[DC], eb[DC];
+    Key kmins[DC], kmaxs[DC];
     unsigned ncmask = 0;
 #pragma unroll
     for (int d = 0; d < DC; d++) {
@@ -952,6 +959,8 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
             kmn = a < kmn ? a : kmn;
             kmx = b > kmx ? b : kmx;
         }
+        kmins[d] = kmn;
+        kmaxs[d] = kmx;
         if (kmn == kmx) continue;
         ncmask |= 1u << d;
         s1 = warp_sum(s1);
@@ -1004,7 +1013,11 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     }
     Key ks, nxt;
     int lt, eq;
-    warp_select<T>(cs + best * ts, pm, n, n / 2, hist, ks, lt, eq, nxt);
+    Key bmin = kmins[0], bmax = kmaxs[0];
+#pragma unroll
+    for (int d = 1; d < DC; d++)
+        if (d == best) { bmin = kmins[d]; bmax = kmaxs[d]; }
+    warp_select<T>(cs + best * ts, pm, n, n / 2, hist, bmin, bmax, ks, lt, eq, nxt);
     const int cumA = lt, cumB = lt + eq;
     bool pickB;
     if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
