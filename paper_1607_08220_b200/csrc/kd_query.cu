@@ -27,7 +27,7 @@
 
 namespace kdb {
 
-constexpr int QCAP = 64;  // traversal stack capacity (tree depth + 2)
+constexpr int QCAP = 40;  // traversal stack capacity (tree depth + 2)
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
 // (measured 34 vs 44 ms on C2); in higher dimensions the binary64 leaf scan dominates and it pays off
 template <int DT>
@@ -325,7 +325,8 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
               const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
               const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
               const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
-              int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
+              int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter,
+              bool push_free_first) {
     constexpr int DC = Dims<DT>::cap;
     constexpr int POOL = 64;
     const int D = DT > 0 ? DT : dims_rt;
@@ -348,6 +349,8 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     float st_off[QCAP][DC];
     int sp = 0;
     int node = -1;
+    int home = -1;          // home leaf: scanned by the first (push-free) descent
+    bool first = false;     // in the first descent (no far children pushed yet)
     long long pool_base = 0;
     int pool_left = 0;
     bool exhausted = false;
@@ -428,6 +431,8 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                     thr32 = make_thr(radius);
                 }
                 sp = 0;
+                home = -1;
+                first = push_free_first;
 #pragma unroll
                 for (int d = 0; d < DC; d++) off[d] = 0.0f;
                 node = n_nodes > 0 ? 0 : -2;  // -2: finished immediately (empty tree)
@@ -447,6 +452,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
         for (;;) {
             c0++;
             const KdNode rec = nodes[node];
+            if (rec.db < 0 && node == home) break;  // already scanned by the first descent
             if (rec.db < 0) {
                 // ---- scan the bucket
                 const int start = rec.a, len = -1 - rec.db;
@@ -509,13 +515,22 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 fo[d] = (d == dim) ? ad : off[d];
                 if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
             }
-            if (admissible(fb) && sp < QCAP) {
+            if (!first && admissible(fb) && sp < QCAP) {
                 st_node[sp] = far;
 #pragma unroll
                 for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
                 sp++;
             }
             node = near;
+        }
+        // ---- after the home leaf: restart from the root with a real k-th distance
+        if (first) {
+            first = false;
+            home = node;
+            node = 0;
+#pragma unroll
+            for (int d = 0; d < DC; d++) off[d] = 0.0f;
+            if (home != 0) continue;  // (a single-leaf tree is done)
         }
         // ---- next admissible far child, or finish
         node = -1;
@@ -574,6 +589,16 @@ __global__ void k_leaf_of(const KdNode* __restrict__ nodes, int64_t n_nodes, con
     val[i] = (int32_t)i;
 }
 
+// first descent without pushes, then a restart from the root with the k-th
+// distance of the home leaf (KDB_KNN_PFF=0 disables; for A/B measurements)
+static bool knn_push_free_first() {
+    static const bool v = [] {
+        const char* e = getenv("KDB_KNN_PFF");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 template <typename T, int DT, int KM>
 static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, const uint32_t* home,
                        cudaStream_t st) {
@@ -592,7 +617,7 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
             k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
                 t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
-                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
+                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, knn_push_free_first());
             cudaFreeAsync(ctr, st);
             return;
         }

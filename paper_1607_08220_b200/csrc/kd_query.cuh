@@ -23,7 +23,7 @@ struct KnnArgs {
     bool thread_per_query = false;  // one-thread-per-query traversal (k > 32 always uses it)
 };
 
-constexpr int KNN_MAX_DEPTH = 61;  // traversal stack capacity - 3
+constexpr int KNN_MAX_DEPTH = 37;  // traversal stack capacity - 3
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st);
 
