@@ -200,42 +200,247 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
         const int j = r * 32 + lane;
         kv[r] = j < m ? tkey(row[picked[j]]) : ~(Key)0;
     }
-    warp_sort<32>(kv);
-    // np.unique: first element of each run of equal keys; boundary index = rank of run
+    warp_sort_t<32>(kv);
+    // np.unique: first element of each run of equal keys; boundary index = rank of run.
+    // Sorted element s = lane*32 + r.
     const int mid = m / 2;
-    int nb = 0, cle = 0;
+    const Key kup = __shfl_up_sync(FULL, kv[31], 1);
+    unsigned fmask = 0;  // bit r: element (lane, r) starts a run
+    int cle_l = 0;
 #pragma unroll
     for (int r = 0; r < 32; r++) {
-        const int s = r * 32 + lane;
-        Key prev = __shfl_up_sync(FULL, kv[r], 1);
-        const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
-        if (lane == 0) prev = lp;
+        const int s = lane * 32 + r;
+        const Key prev = sorted_prev<32>(kv, r, lane, kup, kv[0]);
         const bool first = s < m && (s == 0 || kv[r] != prev);
-        nb += __popc(__ballot_sync(FULL, first));
-        cle += __popc(__ballot_sync(FULL, first && s <= mid));  // run holding sorted position `mid`
+        fmask |= (unsigned)first << r;
+        cle_l += first && s <= mid;  // runs starting at or before sorted position `mid`
     }
+    const int nf = __popc(fmask);
+    int incl = nf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int nb = __shfl_sync(FULL, incl, 31);
+    const int cle = warp_isum(cle_l);
     const int center = cle - 1;
     int wlo = max(0, center - WIN / 2);
     const int whi = min(nb, wlo + WIN);
     wlo = max(0, whi - WIN);
     Split* sp = split + ni;
     T* wbn = wb + (int64_t)ni * WIN;
-    int run = 0;
+    {
+        int bi = incl - nf;  // runs before this lane
 #pragma unroll
-    for (int r = 0; r < 32; r++) {
-        const int s = r * 32 + lane;
-        Key prev = __shfl_up_sync(FULL, kv[r], 1);
-        const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
-        if (lane == 0) prev = lp;
-        const bool first = s < m && (s == 0 || kv[r] != prev);
-        const unsigned bal = __ballot_sync(FULL, first);
-        const int bi = run + __popc(bal & ((1u << lane) - 1));
-        if (first && bi >= wlo && bi < whi) wbn[bi - wlo] = key_inv(kv[r], (T*)nullptr);
-        run += __popc(bal);
+        for (int r = 0; r < 32; r++) {
+            if ((fmask >> r) & 1u) {
+                if (bi >= wlo && bi < whi) wbn[bi - wlo] = key_inv(kv[r], (T*)nullptr);
+                bi++;
+            }
+        }
     }
     uint32_t* wfn = wf + (int64_t)ni * WIN;
     for (int i = lane; i < WIN; i += 32) wfn[i] = 0;
     if (lane == 0) {
+        sp->status = ST_SAMPLED;
+        sp->dim = d0;
+        sp->nb = nb;
+        sp->wlo = wlo;
+        sp->whi = whi;
+        sp->value = 0.0;
+        sp->nl = 0;
+        sp->L = 0ULL;
+    }
+}
+
+// ============================================================================
+// k_sample_cta: the same split choice as k_sample with one 1024-thread CTA per
+// node (one sample element per thread) -- for the shallow levels, where a
+// level has too few nodes to fill the GPU with warps and a warp per node is
+// latency bound (gathers from a node spanning up to the whole point set).
+// ============================================================================
+constexpr int CTA_S = 1024;
+
+// ascending sort of one key per thread over the block (flip-bitonic network;
+// strides < 32 by shuffles, larger ones through two ping-pong shared buffers,
+// one barrier per shared stage).  Returns the buffer holding the sorted keys.
+template <typename K>
+__device__ K* block_sort(K key, K* a, K* b) {
+    const int tid = threadIdx.x;
+    K* buf[2] = {a, b};
+    int pb = 0;
+    for (int ks = 2; ks <= CTA_S; ks <<= 1) {
+        for (int j = ks >> 1; j > 0; j >>= 1) {
+            const int pm = j == (ks >> 1) ? ks - 1 : j;  // flip stage first, then half-cleaners
+            const bool lower = (tid & j) == 0;
+            K o;
+            if (pm < 32) {
+                o = __shfl_xor_sync(FULL, key, pm);
+            } else {
+                buf[pb][tid] = key;
+                __syncthreads();
+                o = buf[pb][tid ^ pm];
+                pb ^= 1;
+            }
+            key = lower ? kmin(key, o) : kmax(key, o);
+        }
+    }
+    buf[pb][tid] = key;
+    __syncthreads();
+    return buf[pb];
+}
+
+// partial Fisher-Yates (median.py:74-85) with one step per thread: sort the
+// (target, step) keys, then resolve "latest earlier step on this slot" chains.
+template <typename FK>
+__device__ void cta_fy(uint32_t n, int m, uint64_t seed, FK* ka, FK* kb, uint32_t* picked) {
+    const int tid = threadIdx.x;
+    FK key = ~(FK)0;
+    if (tid < m) {
+        const uint64_t z = rng_at(seed, (uint64_t)tid);
+        const uint32_t tgt = (uint32_t)tid + (uint32_t)mod_u64_u32(z, n - (uint32_t)tid);
+        key = ((FK)tgt << 10) | (FK)tid;
+    }
+    const FK* sk = block_sort<FK>(key, ka, kb);
+    const FK k = sk[tid];
+    if (k != ~(FK)0) {
+        const uint32_t j = (uint32_t)(k & 1023);
+        const uint32_t tgt = (uint32_t)(k >> 10);
+        const FK prev = tid > 0 ? sk[tid - 1] : ~(FK)0;
+        uint32_t val = tgt;
+        if (tid > 0 && (uint32_t)(prev >> 10) == tgt) {
+            uint32_t t = (uint32_t)(prev & 1023);
+            for (;;) {
+                const FK probe = ((FK)t << 10) | (FK)t;
+                int lo = 0, hi = CTA_S;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sk[mid] < probe) lo = mid + 1; else hi = mid;
+                }
+                if (lo > 0 && (uint32_t)(sk[lo - 1] >> 10) == t) { t = (uint32_t)(sk[lo - 1] & 1023); continue; }
+                break;
+            }
+            val = t;
+        }
+        picked[j] = val;
+    }
+    __syncthreads();
+}
+
+// binary64 block sum (fixed tree order; every warp reduces the partials itself)
+__device__ __forceinline__ double block_sum(double x, double* red) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    x = warp_sum(x);
+    if (lane == 0) red[warp] = x;
+    __syncthreads();
+    const double y = warp_sum(red[lane]);
+    __syncthreads();
+    return y;
+}
+
+template <typename T, int DT>
+__global__ void __launch_bounds__(CTA_S, 1)
+k_sample_cta(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Split* split,
+             T* __restrict__ wb, uint32_t* __restrict__ wf) {
+    __shared__ uint64_t ka[CTA_S], kb[CTA_S];
+    __shared__ uint32_t picked[CTA_S];
+    __shared__ double red[32];
+    __shared__ double s_s2[16], s_eb[16];
+    __shared__ int ired[32];
+    __shared__ int s_cle;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ni = blockIdx.x;
+    const LNode nd = nodes[ni];
+    const uint32_t n = (uint32_t)nd.n;
+    const bool big = n > (1u << 22);
+    const int D = DT > 0 ? DT : c.dims;
+    const int64_t N = c.N;
+
+    // --- variance sample (local_tree.py:122-132)
+    const int take = (int)min((int64_t)n, c.vs);
+    const uint64_t vseed = node_seed(c.seed, nd.path, 0);
+    if (big) cta_fy<uint64_t>(n, take, vseed, ka, kb, picked);
+    else cta_fy<uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked);
+    const bool act = tid < take;
+    const uint32_t pj = act ? picked[tid] : 0u;
+    int d0 = 0;
+    double b0 = 0.0, e0 = 0.0;
+    for (int d = 0; d < D; d++) {
+        const T* row = src + (int64_t)d * N + nd.start;
+        const double x = act ? (double)row[pj] : 0.0;
+        const double s1 = block_sum(x, red);
+        const double sa = block_sum(fabs(x), red);
+        const double mean = __ddiv_rn(s1, (double)take);
+        const double df = act ? __dsub_rn(x, mean) : 0.0;
+        const double s2 = block_sum(__dmul_rn(df, df), red);
+        const double eb = ssd_bound(s2, sa, take);
+        if (tid == 0) { s_s2[d] = s2; s_eb[d] = eb; }
+        if (d == 0 || s2 > b0) { d0 = d; b0 = s2; e0 = eb; }
+    }
+    __syncthreads();
+    bool certified = true;
+    for (int d = 0; d < D; d++)
+        if (d != d0 && !(b0 - s_s2[d] > e0 + s_eb[d])) certified = false;
+    if (!certified) {
+        // exact sequential recomputation in draw order (rare: near-ties)
+        if (tid < D) {
+            const T* row = src + (int64_t)tid * N + nd.start;
+            double mean = 0.0;
+            for (int j = 0; j < take; j++) mean = __dadd_rn(mean, (double)row[picked[j]]);
+            mean = __ddiv_rn(mean, (double)take);
+            double s = 0.0;
+            for (int j = 0; j < take; j++) {
+                const double df = __dsub_rn((double)row[picked[j]], mean);
+                s = __dadd_rn(s, __dmul_rn(df, df));
+            }
+            red[tid] = s;
+        }
+        __syncthreads();
+        d0 = 0;
+        double best = red[0];
+        for (int d = 1; d < D; d++) {
+            const double e = red[d];
+            if (-e < -best) { best = e; d0 = d; }  // np.argsort(-ssd, mergesort)[0]
+        }
+    }
+    __syncthreads();
+
+    // --- median sample of dim d0 (local_tree.py:149-156)
+    const int m = (int)min((int64_t)n, c.ms);
+    const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
+    if (big) cta_fy<uint64_t>(n, m, mseed, ka, kb, picked);
+    else cta_fy<uint32_t>(n, m, mseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked);
+    typedef typename KeyOf<T>::type Key;
+    const T* row = src + (int64_t)d0 * N + nd.start;
+    const Key key = tid < m ? tkey(row[picked[tid]]) : ~(Key)0;
+    const Key* sk = block_sort<Key>(key, reinterpret_cast<Key*>(ka), reinterpret_cast<Key*>(kb));
+    const Key kk = sk[tid];
+    const bool first = tid < m && (tid == 0 || kk != sk[tid > 0 ? tid - 1 : 0]);
+    const unsigned bal = __ballot_sync(FULL, first);
+    if (lane == 0) ired[warp] = __popc(bal);
+    __syncthreads();
+    const int wcnt = ired[lane];
+    int incl = wcnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int nb = __shfl_sync(FULL, incl, 31);
+    const int wbase = __shfl_sync(FULL, incl - wcnt, warp);
+    const int bi = wbase + __popc(bal & ((1u << lane) - 1));  // boundary index of this run
+    const int mid = m / 2;
+    if (tid == mid) s_cle = bi + (first ? 1 : 0);  // runs starting at or before sorted position `mid`
+    __syncthreads();
+    const int center = s_cle - 1;
+    int wlo = max(0, center - WIN / 2);
+    const int whi = min(nb, wlo + WIN);
+    wlo = max(0, whi - WIN);
+    if (first && bi >= wlo && bi < whi) wb[(int64_t)ni * WIN + bi - wlo] = key_inv(kk, (T*)nullptr);
+    if (tid < WIN) wf[(int64_t)ni * WIN + tid] = 0;
+    if (tid == 0) {
+        Split* sp = split + ni;
         sp->status = ST_SAMPLED;
         sp->dim = d0;
         sp->nb = nb;
@@ -480,19 +685,27 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
                     const int j = r * 32 + lane;
                     kv[r] = j < m ? tkey(row[picked[j]]) : ~(Key)0;
                 }
-                warp_sort<32>(kv);
-                int nbr = 0;
+                warp_sort_t<32>(kv);
+                const Key kup = __shfl_up_sync(FULL, kv[31], 1);
+                unsigned fmask = 0;
 #pragma unroll
                 for (int r = 0; r < 32; r++) {
-                    const int s = r * 32 + lane;
-                    Key prev = __shfl_up_sync(FULL, kv[r], 1);
-                    const Key lp = __shfl_sync(FULL, kv[r > 0 ? r - 1 : 0], 31);
-                    if (lane == 0) prev = lp;
-                    const bool first = s < m && (s == 0 || kv[r] != prev);
-                    const unsigned bal = __ballot_sync(FULL, first);
-                    if (first) sb[nbr + __popc(bal & ((1u << lane) - 1))] = key_inv(kv[r], (T*)nullptr);
-                    nbr += __popc(bal);
+                    const int s = lane * 32 + r;
+                    const Key prev = sorted_prev<32>(kv, r, lane, kup, kv[0]);
+                    fmask |= (unsigned)(s < m && (s == 0 || kv[r] != prev)) << r;
                 }
+                const int nf = __popc(fmask);
+                int incl = nf;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int nbr = __shfl_sync(FULL, incl, 31);
+                int bi = incl - nf;
+#pragma unroll
+                for (int r = 0; r < 32; r++)
+                    if ((fmask >> r) & 1u) sb[bi++] = key_inv(kv[r], (T*)nullptr);
                 if (lane == 0) s_nb = nbr;
             }
             __syncthreads();
@@ -1381,6 +1594,11 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));
+    // levels with at most this many nodes choose splits with a CTA per node (KDB_SAMPLE_CTA_K overrides)
+    static const int sample_cta_max = [] {
+        const char* e = std::getenv("KDB_SAMPLE_CTA_K");
+        return e ? atoi(e) : 1024;
+    }();
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
     int64_t max_node = n;  // largest node of the current level (read back with the level counters)
@@ -1414,7 +1632,10 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         uint32_t* tile_left = dalloc<uint32_t>(tiles + 1, st);
         uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
         KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
-        {
+        if (K <= sample_cta_max) {
+            if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(buf[par], lv, c, split, wb, wf);
+            else k_sample_cta<T, 0><<<K, CTA_S, 0, st>>>(buf[par], lv, c, split, wb, wf);
+        } else {
             const unsigned sg = (unsigned)((K + SAMPLE_WARPS - 1) / SAMPLE_WARPS);
             if (dims == 3) {
                 k_sample<T, 3, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(buf[par], lv, K, c, split, wb, wf);

@@ -1,8 +1,8 @@
 // kd_warp.cuh -- warp-level building blocks for the exact split selection.
 //
-//  * warp_sort<R>(keys)  : bitonic sort of 32*R keys held striped in registers
-//                          (element i = r*32 + lane), shuffles for lane strides,
-//                          compile-time register pairs for register strides.
+//  * warp_sort_t<R>(keys): sorting network on 32*R keys held transposed in
+//                          registers (element i = lane*R + r), compile-time
+//                          register pairs for strides < R, shuffles above.
 //  * fy_resolve()        : the partial Fisher-Yates draw of median.py:74-85
 //                          (m distinct positions of [0,n) from SplitMix64),
 //                          computed in parallel: sort (target, step) pairs, then
@@ -21,61 +21,90 @@ __device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
 template <typename K>
 __device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
 
-template <int JR, int R, typename K>
-__device__ __forceinline__ void reg_stage(K (&v)[R], int k, int lane) {
+// compare-exchange: min to a, max to b
+template <typename K>
+__device__ __forceinline__ void cex(K& a, K& b) {
+    const K lo = kmin(a, b), hi = kmax(a, b);
+    a = lo;
+    b = hi;
+}
+
+// Sorting network on 32*R keys held TRANSPOSED in registers: element
+// i = lane*R + r.  Flip-bitonic formulation (every comparator ascending, no
+// direction bits): merge size KS starts with a flip stage (partner i ^ (KS-1))
+// followed by half-cleaners (partner i ^ J).  Strides below R are register
+// pairs (2 instructions per pair, compile-time indices); strides >= R are lane
+// strides (one shuffle per key).  For R = 32: 40 register stages + 15 shuffle
+// stages.
+template <int KS, int R, typename K>
+__device__ __forceinline__ void flip_stage(K (&v)[R], int lane) {
+    if constexpr (KS <= R) {
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-        if ((r & JR) == 0 && (r | JR) < R) {
-            const int i = r * 32 + lane;
-            const bool up = (i & k) == 0;
-            K a = v[r], b = v[r | JR];
-            if ((a > b) == up) { v[r] = b; v[r | JR] = a; }
+        for (int r = 0; r < R; r++) {
+            const int p = r ^ (KS - 1);
+            if (r < p) cex(v[r], v[p]);
+        }
+    } else {
+        constexpr int LM = KS / R - 1;  // partner of (lane, r) is (lane ^ LM, R-1-r)
+        const bool lower = (lane & (KS / R / 2)) == 0;
+#pragma unroll
+        for (int r = 0; r < (R + 1) / 2; r++) {
+            const int q = R - 1 - r;
+            const K a = __shfl_xor_sync(FULL, v[q], LM);  // partner's v[R-1-r]
+            if (q != r) {
+                const K b = __shfl_xor_sync(FULL, v[r], LM);  // partner's v[r], pairs with my v[q]
+                v[q] = lower ? kmin(v[q], b) : kmax(v[q], b);
+            }
+            v[r] = lower ? kmin(v[r], a) : kmax(v[r], a);
         }
     }
 }
 
-// ascending bitonic sort of 32*R keys (R a power of two <= 32)
-template <int R, typename K>
-__device__ __forceinline__ void warp_sort(K (&v)[R]) {
-    const int lane = threadIdx.x & 31;
-    constexpr int N = R * 32;
-    for (int k = 2; k <= N; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j < 32) {
-                const bool lower = (lane & j) == 0;
+template <int J, int R, typename K>
+__device__ __forceinline__ void half_stages(K (&v)[R], int lane) {
+    if constexpr (J >= 1) {
+        if constexpr (J < R) {
 #pragma unroll
-                for (int r = 0; r < R; r++) {
-                    const int i = r * 32 + lane;
-                    const bool up = (i & k) == 0;
-                    K o = __shfl_xor_sync(FULL, v[r], j);
-                    v[r] = (lower == up) ? kmin(v[r], o) : kmax(v[r], o);
-                }
-            } else {
-                switch (j >> 5) {
-                    case 1: reg_stage<1>(v, k, lane); break;
-                    case 2: reg_stage<2>(v, k, lane); break;
-                    case 4: reg_stage<4>(v, k, lane); break;
-                    case 8: reg_stage<8>(v, k, lane); break;
-                    case 16: reg_stage<16>(v, k, lane); break;
-                    default: break;
-                }
+            for (int r = 0; r < R; r++)
+                if ((r & J) == 0) cex(v[r], v[r | J]);
+        } else {
+            constexpr int LM = J / R;
+            const bool lower = (lane & LM) == 0;
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const K o = __shfl_xor_sync(FULL, v[r], LM);
+                v[r] = lower ? kmin(v[r], o) : kmax(v[r], o);
             }
         }
+        half_stages<J / 2, R>(v, lane);
     }
 }
 
-// element i (runtime) of a striped register array, broadcast to all lanes
-template <int R, typename K>
-__device__ __forceinline__ K warp_get(const K (&v)[R], int i) {
-    K out = 0;
-    const int rr = i >> 5, ll = i & 31;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        K t = __shfl_sync(FULL, v[r], ll);
-        if (r == rr) out = t;
+template <int KS, int N, int R, typename K>
+__device__ __forceinline__ void merges(K (&v)[R], int lane) {
+    if constexpr (KS <= N) {
+        flip_stage<KS, R>(v, lane);
+        half_stages<KS / 4, R>(v, lane);
+        merges<KS * 2, N, R>(v, lane);
     }
-    return out;
 }
+
+// ascending sort of 32*R keys (R a power of two <= 32); result transposed:
+// sorted element s sits in lane s / R, register s % R
+template <int R, typename K>
+__device__ __forceinline__ void warp_sort_t(K (&v)[R]) {
+    merges<2, 32 * R, R>(v, threadIdx.x & 31);
+}
+
+// the sorted element before (lane, r) in a transposed sorted array; `up` is
+// __shfl_up_sync(v[R-1], 1) (the previous lane's last key), `none` for element 0
+template <int R, typename K>
+__device__ __forceinline__ K sorted_prev(const K (&v)[R], int r, int lane, K up, K none) {
+    return r > 0 ? v[r > 0 ? r - 1 : 0] : (lane > 0 ? up : none);
+}
+
+// bank-conflict-free shared-memory slot of logical index s (bijection on each 32-word row)
+__device__ __forceinline__ int swz(int s) { return s ^ ((s >> 5) & 31); }
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -118,20 +147,21 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
             v[r] = ~(K)0;
         }
     }
-    warp_sort<R>(v);
+    warp_sort_t<R>(v);
 #pragma unroll
-    for (int r = 0; r < R; r++) skeys[r * 32 + lane] = v[r];
+    for (int r = 0; r < R; r++) skeys[swz(lane * R + r)] = v[r];
     __syncwarp();
     const int M = R * 32;
+    const K up = __shfl_up_sync(FULL, v[R - 1], 1);
 #pragma unroll
     for (int r = 0; r < R; r++) {
-        const int s = r * 32 + lane;
+        const int s = lane * R + r;
         const K key = v[r];
+        const K prev = sorted_prev<R>(v, r, lane, up, ~(K)0);
         if (key == ~(K)0) continue;
         const uint32_t j = (uint32_t)(key & 1023);
         const uint32_t tgt = (uint32_t)(key >> 10);
         uint32_t val;
-        const K prev = s > 0 ? skeys[s - 1] : ~(K)0;
         if (s == 0 || (uint32_t)(prev >> 10) != tgt) {
             val = tgt;  // first step to target this slot: it still holds its own index
         } else {
@@ -143,133 +173,19 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
                 int lo = 0, hi = M;  // lower_bound(probe)
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (skeys[mid] < probe) lo = mid + 1; else hi = mid;
+                    if (skeys[swz(mid)] < probe) lo = mid + 1; else hi = mid;
                 }
-                if (lo > 0 && (uint32_t)(skeys[lo - 1] >> 10) == t) t = (uint32_t)(skeys[lo - 1] & 1023);
-                else break;
+                if (lo > 0) {
+                    const K pk = skeys[swz(lo - 1)];
+                    if ((uint32_t)(pk >> 10) == t) { t = (uint32_t)(pk & 1023); continue; }
+                }
+                break;
             }
             val = t;
         }
         picked[j] = val;
     }
     __syncwarp();
-}
-
-}  // namespace kdb
-
-namespace kdb {
-
-// ---------------------------------------------------------------------------
-// fy_hash: the same partial Fisher-Yates draw as fy_resolve, resolved with a
-// shared-memory hash table (target slot -> list of steps that targeted it)
-// instead of a sort.  For step j, pred(j) = latest earlier step with the same
-// target; V(t) = value at slot t before step t follows the latest step < t that
-// targeted t.  Lists are unordered; "latest earlier" is a max over the list.
-//   hkey/hhead: FY_HS words each, hnext: m words, out: m words.
-// ---------------------------------------------------------------------------
-constexpr int FY_HS = 2048;
-constexpr uint32_t FY_EMPTY = 0xFFFFFFFFu;
-
-__device__ __forceinline__ uint32_t fy_slot0(uint32_t t) { return (t * 0x9E3779B1u) >> (32 - 11); }
-
-__device__ __forceinline__ int fy_find(const uint32_t* hkey, uint32_t t) {
-    uint32_t s = fy_slot0(t);
-    for (;;) {
-        const uint32_t k = hkey[s];
-        if (k == t) return (int)s;
-        if (k == FY_EMPTY) return -1;
-        s = (s + 1) & (FY_HS - 1);
-    }
-}
-
-// latest step < before in the list of slot s (FY_EMPTY if none)
-__device__ __forceinline__ uint32_t fy_latest(const uint32_t* hhead, const uint32_t* hnext, int s, uint32_t before) {
-    uint32_t best = FY_EMPTY;
-    for (uint32_t x = hhead[s]; x != FY_EMPTY; x = hnext[x])
-        if (x < before && (best == FY_EMPTY || x > best)) best = x;
-    return best;
-}
-
-__device__ __forceinline__ void fy_hash(uint32_t n, int m, uint64_t seed, uint32_t* hkey, uint32_t* hhead, uint32_t* hnext,
-                        uint32_t* out) {
-    const int lane = threadIdx.x & 31;
-    for (int i = lane; i < FY_HS; i += 32) { hkey[i] = FY_EMPTY; hhead[i] = FY_EMPTY; }
-    __syncwarp();
-    for (int j = lane; j < m; j += 32) {
-        const uint64_t z = rng_at(seed, (uint64_t)j);
-        const uint32_t t = (uint32_t)j + (uint32_t)mod_u64_u32(z, n - (uint32_t)j);
-        uint32_t s = fy_slot0(t);
-        for (;;) {
-            const uint32_t old = atomicCAS(&hkey[s], FY_EMPTY, t);
-            if (old == FY_EMPTY || old == t) break;
-            s = (s + 1) & (FY_HS - 1);
-        }
-        hnext[j] = atomicExch(&hhead[s], (uint32_t)j);
-        out[j] = t;
-    }
-    __syncwarp();
-    for (int j = lane; j < m; j += 32) {
-        const uint32_t t = out[j];
-        uint32_t cur = fy_latest(hhead, hnext, fy_find(hkey, t), (uint32_t)j);
-        uint32_t val = t;
-        if (cur != FY_EMPTY) {
-            for (;;) {  // V(cur): value at slot cur before step cur
-                const int s2 = fy_find(hkey, cur);
-                const uint32_t p = s2 < 0 ? FY_EMPTY : fy_latest(hhead, hnext, s2, cur);
-                if (p == FY_EMPTY) { val = cur; break; }
-                cur = p;
-            }
-        }
-        out[j] = val;
-    }
-    __syncwarp();
-}
-
-// ---------------------------------------------------------------------------
-// warp_radix_sort: stable LSD radix sort (8-bit digits) of m keys held in
-// shared memory (a -> sorted in a; b is scratch of m keys; cnt is 256 words).
-// Within a 32-key chunk, equal digits keep lane order via __match_any_sync.
-// ---------------------------------------------------------------------------
-template <typename K>
-__device__ void warp_radix_sort(K* a, K* b, int m, uint32_t* cnt) {
-    const int lane = threadIdx.x & 31;
-    constexpr int KB = sizeof(K) * 8;
-    for (int shift = 0; shift < KB; shift += 8) {
-        for (int i = lane; i < 256; i += 32) cnt[i] = 0;
-        __syncwarp();
-        for (int i = lane; i < m; i += 32) atomicAdd(&cnt[(int)((a[i] >> shift) & 255)], 1u);
-        __syncwarp();
-        // exclusive scan of the 256 counters (8 per lane)
-        uint32_t h[8], s = 0;
-#pragma unroll
-        for (int j = 0; j < 8; j++) { h[j] = cnt[lane * 8 + j]; s += h[j]; }
-        uint32_t incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        uint32_t run = incl - s;
-#pragma unroll
-        for (int j = 0; j < 8; j++) { cnt[lane * 8 + j] = run; run += h[j]; }
-        __syncwarp();
-        for (int c = 0; c < m; c += 32) {
-            const int i = c + lane;
-            const bool v = i < m;
-            const K key = v ? a[i] : (K)0;
-            const uint32_t dg = v ? (uint32_t)((key >> shift) & 255) : 256u + lane;
-            const unsigned peers = __match_any_sync(FULL, dg);
-            const int r = __popc(peers & ((1u << lane) - 1));
-            const uint32_t base = v ? cnt[dg] : 0;
-            __syncwarp();
-            if (v) b[base + r] = key;
-            if (v && r == 0) cnt[dg] = base + __popc(peers);
-            __syncwarp();
-        }
-        { K* t = a; a = b; b = t; }  // result now in `a` (pointer swap)
-        __syncwarp();
-    }
-    // KB/8 passes: an even number for 32- and 64-bit keys, so the data ends in the caller's `a`
 }
 
 }  // namespace kdb
