@@ -123,13 +123,14 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     typedef typename std::conditional<BIG, uint64_t, uint32_t>::type FK;
     FK* skeys = reinterpret_cast<FK*>(smem_raw) + warp * MAXS;
     uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * sizeof(FK)) + warp * MAXS;
+    uint16_t* gidx = reinterpret_cast<uint16_t*>(smem_raw + SAMPLE_WARPS * MAXS * (sizeof(FK) + 4)) + warp * MAXS;
     const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
 
     // --- variance sample (local_tree.py:122-132)
     const int take = (int)min((int64_t)n, c.vs);
     const uint64_t vseed = node_seed(c.seed, nd.path, 0);
-    fy_resolve<32, FK>(n, take, vseed, skeys, picked);
+    fy_resolve<32, FK>(n, take, vseed, skeys, picked, gidx);
 
     int d0 = 0;
     double b0 = 0.0, e0 = 0.0;
@@ -191,7 +192,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const int m = (int)min((int64_t)n, c.ms);
     const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
     __syncwarp();
-    fy_resolve<32, FK>(n, m, mseed, skeys, picked);
+    fy_resolve<32, FK>(n, m, mseed, skeys, picked, gidx);
     typedef typename KeyOf<T>::type Key;
     const T* row = src + (int64_t)d0 * N + nd.start;
     Key kv[32];
@@ -294,7 +295,7 @@ __device__ K* block_sort(K key, K* a, K* b) {
 // partial Fisher-Yates (median.py:74-85) with one step per thread: sort the
 // (target, step) keys, then resolve "latest earlier step on this slot" chains.
 template <typename FK>
-__device__ void cta_fy(uint32_t n, int m, uint64_t seed, FK* ka, FK* kb, uint32_t* picked) {
+__device__ void cta_fy(uint32_t n, int m, uint64_t seed, FK* ka, FK* kb, uint32_t* picked, uint16_t* gidx) {
     const int tid = threadIdx.x;
     FK key = ~(FK)0;
     if (tid < m) {
@@ -304,22 +305,29 @@ __device__ void cta_fy(uint32_t n, int m, uint64_t seed, FK* ka, FK* kb, uint32_
     }
     const FK* sk = block_sort<FK>(key, ka, kb);
     const FK k = sk[tid];
+    const FK prev = tid > 0 ? sk[tid - 1] : ~(FK)0;
+    const uint32_t tgt = (uint32_t)(k >> 10);
+    // gidx[t]: sorted index of the first step that targets slot t < CTA_S
+    gidx[tid] = 0xFFFF;
+    __syncthreads();
+    if (k != ~(FK)0 && tgt < (uint32_t)CTA_S && (tid == 0 || (uint32_t)(prev >> 10) != tgt)) gidx[tgt] = (uint16_t)tid;
+    __syncthreads();
     if (k != ~(FK)0) {
         const uint32_t j = (uint32_t)(k & 1023);
-        const uint32_t tgt = (uint32_t)(k >> 10);
-        const FK prev = tid > 0 ? sk[tid - 1] : ~(FK)0;
         uint32_t val = tgt;
         if (tid > 0 && (uint32_t)(prev >> 10) == tgt) {
             uint32_t t = (uint32_t)(prev & 1023);
-            for (;;) {
-                const FK probe = ((FK)t << 10) | (FK)t;
-                int lo = 0, hi = CTA_S;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sk[mid] < probe) lo = mid + 1; else hi = mid;
+            for (;;) {  // latest step < t that targeted slot t
+                int g = gidx[t];
+                if (g == 0xFFFF) break;
+                uint32_t best = 0xFFFFFFFFu;
+                for (; g < CTA_S; g++) {
+                    const FK gk = sk[g];
+                    if ((uint32_t)(gk >> 10) != t || (uint32_t)(gk & 1023) >= t) break;
+                    best = (uint32_t)(gk & 1023);
                 }
-                if (lo > 0 && (uint32_t)(sk[lo - 1] >> 10) == t) { t = (uint32_t)(sk[lo - 1] & 1023); continue; }
-                break;
+                if (best == 0xFFFFFFFFu) break;
+                t = best;
             }
             val = t;
         }
@@ -345,6 +353,7 @@ k_sample_cta(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx 
              T* __restrict__ wb, uint32_t* __restrict__ wf) {
     __shared__ uint64_t ka[CTA_S], kb[CTA_S];
     __shared__ uint32_t picked[CTA_S];
+    __shared__ uint16_t gidx[CTA_S];
     __shared__ double red[32];
     __shared__ double s_s2[16], s_eb[16];
     __shared__ int ired[32];
@@ -360,8 +369,8 @@ k_sample_cta(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx 
     // --- variance sample (local_tree.py:122-132)
     const int take = (int)min((int64_t)n, c.vs);
     const uint64_t vseed = node_seed(c.seed, nd.path, 0);
-    if (big) cta_fy<uint64_t>(n, take, vseed, ka, kb, picked);
-    else cta_fy<uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked);
+    if (big) cta_fy<uint64_t>(n, take, vseed, ka, kb, picked, gidx);
+    else cta_fy<uint32_t>(n, take, vseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked, gidx);
     const bool act = tid < take;
     const uint32_t pj = act ? picked[tid] : 0u;
     int d0 = 0;
@@ -409,8 +418,8 @@ k_sample_cta(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx 
     // --- median sample of dim d0 (local_tree.py:149-156)
     const int m = (int)min((int64_t)n, c.ms);
     const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
-    if (big) cta_fy<uint64_t>(n, m, mseed, ka, kb, picked);
-    else cta_fy<uint32_t>(n, m, mseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked);
+    if (big) cta_fy<uint64_t>(n, m, mseed, ka, kb, picked, gidx);
+    else cta_fy<uint32_t>(n, m, mseed, reinterpret_cast<uint32_t*>(ka), reinterpret_cast<uint32_t*>(kb), picked, gidx);
     typedef typename KeyOf<T>::type Key;
     const T* row = src + (int64_t)d0 * N + nd.start;
     const Key key = tid < m ? tkey(row[picked[tid]]) : ~(Key)0;
@@ -1588,8 +1597,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int ntasks_known = K == 0 ? 1 : 0;
     {
     }
-    const size_t sample_smem32 = (size_t)SAMPLE_WARPS * MAXS * (4 + 4);
-    const size_t sample_smem64 = (size_t)SAMPLE_WARPS * MAXS * (8 + 4);
+    const size_t sample_smem32 = (size_t)SAMPLE_WARPS * MAXS * (4 + 4 + 2);
+    const size_t sample_smem64 = (size_t)SAMPLE_WARPS * MAXS * (8 + 4 + 2);
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));

@@ -132,8 +132,11 @@ __device__ __forceinline__ uint64_t mod_u64_u32(uint64_t z, uint32_t d) {
 // Writes picked[0..m) (node-relative positions) into shared memory.
 // skeys: shared scratch of 32*R entries of type K (K = uint32_t when
 // n <= 2^22, else uint64_t); keys are (target << 10) | step.
+// gidx (optional, 32*R u16): per slot t < 32*R, sorted index of the first step
+// that targets t -- turns each chain hop into one or two shared loads instead of
+// a binary search.
 template <int R, typename K>
-__device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t* picked) {
+__device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t* picked, uint16_t* gidx = nullptr) {
     const int lane = threadIdx.x & 31;
     K v[R];
 #pragma unroll
@@ -150,9 +153,20 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
     warp_sort_t<R>(v);
 #pragma unroll
     for (int r = 0; r < R; r++) skeys[swz(lane * R + r)] = v[r];
-    __syncwarp();
     const int M = R * 32;
     const K up = __shfl_up_sync(FULL, v[R - 1], 1);
+    if (gidx) {
+        for (int i = lane; i < M; i += 32) gidx[i] = 0xFFFF;
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const K prev = sorted_prev<R>(v, r, lane, up, ~(K)0);
+            const uint32_t tgt = (uint32_t)(v[r] >> 10);
+            if (v[r] != ~(K)0 && tgt < (uint32_t)M && (lane * R + r == 0 || (uint32_t)(prev >> 10) != tgt))
+                gidx[tgt] = (uint16_t)(lane * R + r);
+        }
+    }
+    __syncwarp();
 #pragma unroll
     for (int r = 0; r < R; r++) {
         const int s = lane * R + r;
@@ -168,7 +182,20 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
             // value at slot `tgt` before step j = value that step j' moved there =
             // value at slot j' before step j' (V chain)
             uint32_t t = (uint32_t)(prev & 1023);
-            for (;;) {
+            if (gidx) {
+                for (;;) {  // latest step < t that targeted slot t (its group is sorted by step)
+                    int g = gidx[t];
+                    if (g == 0xFFFF) break;
+                    uint32_t best = 0xFFFFFFFFu;
+                    for (; g < M; g++) {
+                        const K gk = skeys[swz(g)];
+                        if ((uint32_t)(gk >> 10) != t || (uint32_t)(gk & 1023) >= t) break;
+                        best = (uint32_t)(gk & 1023);
+                    }
+                    if (best == 0xFFFFFFFFu) break;
+                    t = best;
+                }
+            } else for (;;) {
                 const K probe = ((K)t << 10) | (K)t;
                 int lo = 0, hi = M;  // lower_bound(probe)
                 while (lo < hi) {
