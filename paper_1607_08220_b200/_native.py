@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkdtree_b200.so")
+LIB_PATH = os.environ.get("KDB_LIB_PATH") or os.path.join(_HERE, "libkdtree_b200.so")  # override: A/B builds
 
 KD_OK, KD_EINVAL, KD_ECUDA, KD_EUNSUPPORTED, KD_ENOMEM = 0, -1, -2, -3, -4
 KD_F32, KD_F64 = 1, 2

@@ -470,13 +470,19 @@ __device__ __forceinline__ int tile_node(const LNode* nodes, int K, uint32_t t) 
     return lo;
 }
 
+// tile -> node of the level (once per level, so the tile kernels start with one load)
+__global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32_t tiles, int32_t* __restrict__ tmap) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tiles) tmap[t] = tile_node(nodes, K, t);
+}
+
 // ============================================================================
 // k_hist: windowed histogram (median.py:128-140 restricted to the boundaries
 // around the sampled median; counts below the window are aggregated in L)
 // ============================================================================
 template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
-k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c, Split* split,
+k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c, Split* split,
        const T* __restrict__ wb, uint32_t* __restrict__ wf) {
     constexpr int EPT = TILE / TILE_THREADS;
     constexpr int NW = TILE_THREADS / 32;
@@ -485,7 +491,7 @@ k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx
     __shared__ T q[NW][64];  // per-warp queue of in-window values (keeps the searches warp-dense)
     __shared__ unsigned long long sL;
     const uint32_t t = blockIdx.x;
-    const int ni = tile_node(nodes, K, t);
+    const int ni = tmap[t];
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     const int nw = sp.whi - sp.wlo;
@@ -500,20 +506,20 @@ k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx
         const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
         v[j] = e < e1 ? row[e] : T(0);
     }
+    // sb[i] = boundary i+1 for i < nw-2, +inf above: bin of x = 1 + #{i : sb[i] <= x}
     for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
         sf[i] = 0;
-        if (i < nw) sb[i] = wb[(int64_t)ni * WIN + i];
+        sb[i] = i < nw - 2 ? wb[(int64_t)ni * WIN + i + 1] : T(INFINITY);
     }
     if (threadIdx.x == 0) sL = 0;
+    const T lo_b = wb[(int64_t)ni * WIN], hi_b = wb[(int64_t)ni * WIN + nw - 1];
     __syncthreads();
-    const T lo_b = sb[0], hi_b = sb[nw - 1];
-    auto search = [&](T x) {  // upper_bound of x in sb[1 .. nw-1)
-        int lo = 1, len = nw - 2;
-        while (len > 0) {
-            const int half = len >> 1;
-            if (sb[lo + half] <= x) { lo += half + 1; len -= half + 1; } else { len = half; }
-        }
-        atomicAdd(&sf[lo], 1u);
+    auto search = [&](T x) {  // branchless upper_bound of x in the boundaries 1 .. nw-2
+        int pos = 0;
+#pragma unroll
+        for (int step = WIN / 2; step > 0; step >>= 1)
+            if (sb[pos + step - 1] <= x) pos += step;
+        atomicAdd(&sf[1 + pos], 1u);
     };
     uint32_t lc = 0;
     int qn = 0;  // warp-uniform queue length
@@ -832,12 +838,12 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
 // ============================================================================
 template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
-k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevCtx c,
+k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
         const Split* __restrict__ split, uint32_t* tile_left) {
     constexpr int EPT = TILE / TILE_THREADS;
     __shared__ uint32_t red[TILE_THREADS / 32];
     const uint32_t t = blockIdx.x;
-    const int ni = tile_node(nodes, K, t);
+    const int ni = tmap[t];
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     uint32_t cnt = 0;
@@ -1138,6 +1144,149 @@ __device__ __noinline__ void fy_resolve_n(uint32_t n, uint64_t seed, uint32_t* f
     else fy_resolve<32, uint32_t>(n, (int)n, seed, fk, fp);
 }
 
+// exact max-variance dimension of a whole-node sample (the reference's
+// sequential two-pass sums in Fisher-Yates draw order); rare: near-ties only
+template <typename T>
+__device__ __noinline__ int sub_exact_dim(const T* cs, const uint16_t* pm, int n, int ts, int D, unsigned ncmask,
+                                          uint64_t path, const DevCtx& c, uint32_t* fyslots, int* fylocks) {
+    const int lane = threadIdx.x & 31;
+    const int slot = blockIdx.x % FY_SLOTS;
+    if (lane == 0) while (atomicCAS(&fylocks[slot], 0, 1) != 0) {}
+    __syncwarp();
+    __threadfence();
+    uint32_t* fk = fyslots + (size_t)slot * 2 * MAXS;
+    uint32_t* fp = fk + MAXS;
+    fy_resolve_n((uint32_t)n, node_seed(c.seed, path, 0), fk, fp);
+    double exact = 0.0;
+    if (lane < D && ((ncmask >> lane) & 1u)) {
+        const T* row = cs + lane * ts;
+        double mean = 0.0;
+        for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[pm[fp[j]]]);
+        mean = __ddiv_rn(mean, (double)n);
+        double s = 0.0;
+        for (int j = 0; j < n; j++) {
+            const double df = __dsub_rn((double)row[pm[fp[j]]], mean);
+            s = __dadd_rn(s, __dmul_rn(df, df));
+        }
+        exact = s;
+    }
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) atomicExch(&fylocks[slot], 0);
+    int best = -1;
+    double bv = 0.0;
+    for (int d = 0; d < D; d++) {
+        const double e = __shfl_sync(FULL, exact, d);
+        if (!((ncmask >> d) & 1u)) continue;
+        if (best < 0 || -e < -bv) { best = d; bv = e; }  // stable descending (argsort(-ssd))
+    }
+    return best;
+}
+
+// Small nodes (n <= 32*SR, fixed dimension count): the node's points are read
+// once into registers; per-dimension sums come from registers and the split
+// dimension's keys are sorted by the unrolled network (warp_sort_t) instead of
+// radix-select passes.  Same decisions as sub_split (same certified bound).
+template <typename T, int DT, int SR>
+__device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm, int n, int ts, uint64_t path,
+                                                const DevCtx& c, uint32_t* fyslots, int* fylocks, int& out_dim,
+                                                double& out_val, int& out_nl) {
+    typedef typename KeyOf<T>::type Key;
+    __builtin_assume(__isShared(cs));
+    __builtin_assume(__isShared(pm));
+    const int lane = threadIdx.x & 31;
+    T x[DT][SR];
+#pragma unroll
+    for (int r = 0; r < SR; r++) {
+        const int i = r * 32 + lane;
+        const int q = pm[i < n ? i : 0];
+#pragma unroll
+        for (int d = 0; d < DT; d++) x[d][r] = cs[d * ts + q];
+    }
+    int best = -1;
+    double bs = 0.0, be = 0.0;
+    double s2v[DT], eb[DT];
+    unsigned ncmask = 0;
+#pragma unroll
+    for (int d = 0; d < DT; d++) {
+        s2v[d] = 0.0;
+        eb[d] = 0.0;
+        const double x0 = (double)__shfl_sync(FULL, x[d][0], 0);
+        Key kmn = ~(Key)0, kmx = 0;
+        double s1 = 0.0, sq = 0.0;
+#pragma unroll
+        for (int r = 0; r < SR; r++) {
+            if (r * 32 + lane < n) {
+                const Key k = tkey(x[d][r]);
+                kmn = k < kmn ? k : kmn;
+                kmx = k > kmx ? k : kmx;
+                const double y = __dsub_rn((double)x[d][r], x0);
+                s1 = __dadd_rn(s1, y);
+                sq = __dadd_rn(sq, __dmul_rn(y, y));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const Key a = __shfl_xor_sync(FULL, kmn, o), b = __shfl_xor_sync(FULL, kmx, o);
+            kmn = a < kmn ? a : kmn;
+            kmx = b > kmx ? b : kmx;
+        }
+        if (kmn == kmx) continue;
+        ncmask |= 1u << d;
+        s1 = warp_sum(s1);
+        sq = warp_sum(sq);
+        const double bb = __dmul_rn(s1, s1) / (double)n;
+        s2v[d] = sq - bb;
+        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq + bb) + 1e-300;
+        if (best < 0 || s2v[d] > bs) { best = d; bs = s2v[d]; be = eb[d]; }
+    }
+    out_dim = -1;
+    if (best < 0) return;
+    bool certified = true;
+#pragma unroll
+    for (int d = 0; d < DT; d++)
+        if (d != best && ((ncmask >> d) & 1u) && !(bs - s2v[d] > be + eb[d])) certified = false;
+    if (!certified) best = sub_exact_dim<T>(cs, pm, n, ts, DT, ncmask, path, c, fyslots, fylocks);
+    Key kv[SR];
+#pragma unroll
+    for (int r = 0; r < SR; r++) {
+        T v = x[0][r];
+#pragma unroll
+        for (int d = 1; d < DT; d++)
+            if (d == best) v = x[d][r];
+        kv[r] = r * 32 + lane < n ? tkey(v) : ~(Key)0;
+    }
+    warp_sort_t<SR>(kv);  // sorted element s in lane s / SR, register s % SR
+    const int h = n / 2;
+    Key mine = kv[0];
+#pragma unroll
+    for (int r = 1; r < SR; r++)
+        if (r == h % SR) mine = kv[r];
+    const Key ks = __shfl_sync(FULL, mine, h / SR);
+    int lt = 0, eq = 0;
+    Key nx = ~(Key)0;
+#pragma unroll
+    for (int r = 0; r < SR; r++) {
+        const bool valid = lane * SR + r < n;
+        lt += __popc(__ballot_sync(FULL, valid && kv[r] < ks));
+        eq += __popc(__ballot_sync(FULL, valid && kv[r] == ks));
+        if (valid && kv[r] > ks && kv[r] < nx) nx = kv[r];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const Key on = __shfl_xor_sync(FULL, nx, o);
+        nx = on < nx ? on : nx;
+    }
+    const int cumA = lt, cumB = lt + eq;
+    bool pickB;
+    if (cumA == 0) pickB = true;
+    else if (cumB >= n) pickB = false;
+    else pickB = half_diff(cumB, n) < half_diff(cumA, n);
+    out_dim = best;
+    out_val = pickB ? (double)key_inv(nx, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
+    out_nl = pickB ? cumB : cumA;
+}
+
 template <typename T, int DT>
 __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int dims_rt, uint64_t path,
                           const DevCtx& c, uint32_t* hist, uint32_t* fyslots, int* fylocks, int& out_dim,
@@ -1200,39 +1349,7 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
 #pragma unroll
     for (int d = 0; d < DC; d++)
         if (d != best && ((ncmask >> d) & 1u) && !(bs - s2v[d] > be + eb[d])) certified = false;
-    if (!certified) {
-        // exact: the variance sample is the whole node in Fisher-Yates draw order
-        const int slot = blockIdx.x % FY_SLOTS;
-        if (lane == 0) while (atomicCAS(&fylocks[slot], 0, 1) != 0) {}
-        __syncwarp();
-        __threadfence();
-        uint32_t* fk = fyslots + (size_t)slot * 2 * MAXS;
-        uint32_t* fp = fk + MAXS;
-        fy_resolve_n((uint32_t)n, node_seed(c.seed, path, 0), fk, fp);
-        double exact = 0.0;
-        if (lane < D && ((ncmask >> lane) & 1u)) {
-            const T* row = cs + lane * ts;
-            double mean = 0.0;
-            for (int j = 0; j < n; j++) mean = __dadd_rn(mean, (double)row[pm[fp[j]]]);
-            mean = __ddiv_rn(mean, (double)n);
-            double s = 0.0;
-            for (int j = 0; j < n; j++) {
-                const double df = __dsub_rn((double)row[pm[fp[j]]], mean);
-                s = __dadd_rn(s, __dmul_rn(df, df));
-            }
-            exact = s;
-        }
-        __syncwarp();
-        __threadfence();
-        if (lane == 0) atomicExch(&fylocks[slot], 0);
-        best = -1;
-        double bv = 0.0;
-        for (int d = 0; d < D; d++) {
-            const double e = __shfl_sync(FULL, exact, d);
-            if (!((ncmask >> d) & 1u)) continue;
-            if (best < 0 || -e < -bv) { best = d; bv = e; }  // stable descending (argsort(-ssd))
-        }
-    }
+    if (!certified) best = sub_exact_dim<T>(cs, pm, n, ts, D, ncmask, path, c, fyslots, fylocks);
     Key ks, nxt;
     int lt, eq;
     Key bmin = kmins[0], bmax = kmaxs[0];
@@ -1316,8 +1433,16 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         maxd = max(maxd, rd);
         int dim = -1, nl = 0;
         double val = 0.0;
-        if (nn > c.bucket) sub_split<T, DT>(cs, ((rd & 1) ? perm[1] : perm[0]) + st, nn, ts, D, path, c, hist, fyslots,
-                                            fylocks, dim, val, nl);
+        if (nn > c.bucket) {
+            const uint16_t* pmn = ((rd & 1) ? perm[1] : perm[0]) + st;
+            if constexpr (DT > 0) {
+                if (nn <= 64) sub_split_small<T, DT, 2>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
+                else if (nn <= 128) sub_split_small<T, DT, 4>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
+                else sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
+            } else {
+                sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
+            }
+        }
         if (dim < 0) {
             if (lane == 0) {
                 out_nodes[pre] = KdNode{0.0, (int32_t)(tk.start + st), -1 - nn};
@@ -1654,10 +1779,12 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
                 if (big_levels) k_sample<T, 0, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(buf[par], lv, K, c, split, wb, wf);
             }
         }
-        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, wb, wf);
+        int32_t* tmap = dalloc<int32_t>(tiles, st);
+        k_tile_map<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tiles, tmap);
+        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, tmap, c, split, wb, wf);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(buf[par], lv, c, split, slow_list, slow_count);
-        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, K, c, split, tile_left);
+        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, tmap, c, split, tile_left);
         size_t tmp_bytes = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
@@ -1688,7 +1815,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         slow_total += *h_slow;
         ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
         dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st);
-        dfree(tile_loff, st); dfree(tmp, st);
+        dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
         K = (int)(h_ctr[0] >> 32);
