@@ -1048,7 +1048,6 @@ constexpr int FY_SLOTS = 8192;  // global scratch slots for the rare exact-varia
 __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
     size_t b = (size_t)dims * ts * tsize;
     b = (b + 15) & ~size_t(15);
-    b += (size_t)ts * 4;      // original row ids (the source buffer may be the output)
     b += (size_t)2 * ts * 2;  // perm ping-pong by depth parity
     b = (b + 15) & ~size_t(15);
     b += 256 * 4;             // radix histogram
@@ -1368,7 +1367,7 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
 }
 
 template <typename T, int DT>
-__global__ void __launch_bounds__(32, 12)
+__global__ void __launch_bounds__(32, 13)
 k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0, const int32_t* idx1, DevCtx c,
           KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, SubStack* __restrict__ sstack,
           uint32_t* __restrict__ fyslots, int* __restrict__ fylocks, int32_t* task_nodes, int32_t* task_depth) {
@@ -1404,7 +1403,6 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
     unsigned char* p = smem_raw;
     T* cs = reinterpret_cast<T*>(p); p += (size_t)D * ts * sizeof(T);
     p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
-    int32_t* cidx = reinterpret_cast<int32_t*>(p); p += (size_t)ts * 4;
     uint16_t* perm[2];
     perm[0] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
     perm[1] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
@@ -1412,7 +1410,6 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
     uint32_t* hist = reinterpret_cast<uint32_t*>(p);
     for (int e = lane; e < n; e += 32) {
         for (int d = 0; d < D; d++) cs[d * ts + e] = src[(int64_t)d * N + tk.start + e];
-        cidx[e] = isrc[tk.start + e];
         perm[0][e] = (uint16_t)e;
     }
     __syncwarp();
@@ -1420,7 +1417,7 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         for (int e = lane; e < len; e += 32) {
             const int qv = pm[st + e];
             for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + st + e] = cs[d * ts + qv];
-            idx0[tk.start + st + e] = cidx[qv];
+            if (pm != perm[0]) perm[0][st + e] = (uint16_t)qv;  // final order collects in perm[0]
         }
     };
     // depth-first, left child first: preorder numbering is the visit order
@@ -1487,6 +1484,20 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         nn = nl;
         rd = rd + 1;
         __syncwarp();
+    }
+    // row ids in the final order; the source may alias the output, so read all before writing
+    __syncwarp();
+    int32_t rid[MAXS / 32];
+#pragma unroll
+    for (int k2 = 0; k2 < MAXS / 32; k2++) {
+        const int e = k2 * 32 + lane;
+        if (e < n) rid[k2] = isrc[tk.start + perm[0][e]];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < MAXS / 32; k2++) {
+        const int e = k2 * 32 + lane;
+        if (e < n) idx0[tk.start + e] = rid[k2];
     }
     if (lane == 0) {
         task_nodes[blockIdx.x] = cursor;
