@@ -1366,6 +1366,14 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     out_nl = pickB ? cumB : cumA;
 }
 
+// one element global -> shared without a register round trip (cp.async, 4 or 8 bytes)
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 template <typename T, int DT>
 __global__ void __launch_bounds__(32, 13)
 k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0, const int32_t* idx1, DevCtx c,
@@ -1408,10 +1416,13 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
     perm[1] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
     p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
     uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    // stage the task's points with asynchronous copies (all loads in flight at once)
     for (int e = lane; e < n; e += 32) {
-        for (int d = 0; d < D; d++) cs[d * ts + e] = src[(int64_t)d * N + tk.start + e];
+        for (int d = 0; d < D; d++) cp_async_elem(&cs[d * ts + e], &src[(int64_t)d * N + tk.start + e]);
         perm[0][e] = (uint16_t)e;
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
     auto emit = [&](const uint16_t* pm, int st, int len) {
         for (int e = lane; e < len; e += 32) {
@@ -1460,16 +1471,23 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         const uint16_t* pc = perm[rd & 1];
         uint16_t* pn = perm[(rd + 1) & 1];
         const T* row = cs + dim * ts;
+        const T vt = (T)val;  // the split value is a coordinate: comparing in T is exact
         int lrun = 0;
-        for (int b = 0; b < nn; b += 32) {
-            const int e = b + lane;
-            const bool valid = e < nn;
-            const int qv = valid ? pc[st + e] : 0;
-            const bool f = valid && (double)row[qv] < val;
-            const unsigned bal = __ballot_sync(FULL, f);
-            const int lp = __popc(bal & ((1u << lane) - 1));
-            if (valid) pn[st + (f ? lrun + lp : nl + (e - (lrun + lp)))] = (uint16_t)qv;
-            lrun += __popc(bal);
+        for (int b = 0; b < nn; b += 128) {  // 4 chunks of 32 per round: loads first, then ballots
+            int qv[4];
+            bool f[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) qv[u] = b + u * 32 + lane < nn ? pc[st + b + u * 32 + lane] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) f[u] = b + u * 32 + lane < nn && row[qv[u]] < vt;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = b + u * 32 + lane;
+                const unsigned bal = __ballot_sync(FULL, f[u]);
+                const int lp = __popc(bal & ((1u << lane) - 1));
+                if (e < nn) pn[st + (f[u] ? lrun + lp : nl + (e - (lrun + lp)))] = (uint16_t)qv[u];
+                lrun += __popc(bal);
+            }
         }
         __syncwarp();
         if (lane == 0) {
