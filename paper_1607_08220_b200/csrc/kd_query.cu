@@ -574,19 +574,42 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
 template <int DT>
 __global__ void k_leaf_of(const KdNode* __restrict__ nodes, int64_t n_nodes, const double* __restrict__ queries,
                           int dims_rt, int64_t nq, uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+    // LQ independent descents per thread, advanced in lock step: LQ node loads in flight at once
+    constexpr int LQ = 4;
     const int D = DT > 0 ? DT : dims_rt;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= nq) return;
-    int node = 0;
-    if (n_nodes > 0) {
-        for (;;) {
-            const KdNode rec = nodes[node];
-            if (rec.db < 0) break;
-            node = queries[i * D + rec.db] < rec.v ? node + 1 : rec.a;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int node[LQ];
+    bool live[LQ];
+#pragma unroll
+    for (int u = 0; u < LQ; u++) {
+        node[u] = 0;
+        live[u] = i0 + u * stride < nq && n_nodes > 0;
+    }
+    for (;;) {
+        bool any = false;
+        KdNode rec[LQ];
+#pragma unroll
+        for (int u = 0; u < LQ; u++)
+            if (live[u]) rec[u] = nodes[node[u]];
+#pragma unroll
+        for (int u = 0; u < LQ; u++) {
+            if (!live[u]) continue;
+            if (rec[u].db < 0) { live[u] = false; continue; }
+            const int64_t i = i0 + u * stride;
+            node[u] = queries[i * D + rec[u].db] < rec[u].v ? node[u] + 1 : rec[u].a;
+            any = true;
+        }
+        if (!any) break;
+    }
+#pragma unroll
+    for (int u = 0; u < LQ; u++) {
+        const int64_t i = i0 + u * stride;
+        if (i < nq) {
+            key[i] = (uint32_t)node[u];
+            val[i] = (int32_t)i;
         }
     }
-    key[i] = (uint32_t)node;
-    val[i] = (int32_t)i;
 }
 
 // first descent without pushes, then a restart from the root with the k-th
@@ -660,7 +683,7 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
         KD_CUDA(cudaMallocAsync((void**)&k1, a.nq * 4, st));
         KD_CUDA(cudaMallocAsync((void**)&v0, a.nq * 4, st));
         KD_CUDA(cudaMallocAsync((void**)&order, a.nq * 4, st));
-        const unsigned blocks = (unsigned)((a.nq + 255) / 256);
+        const unsigned blocks = (unsigned)((a.nq + 1023) / 1024);  // 4 queries per thread
         if (t.dims == 3) k_leaf_of<3><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
         else k_leaf_of<0><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
         int bits = 1;
