@@ -910,7 +910,7 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
 #pragma unroll
             for (int d = 0; d < DC; d++)
                 if (d < D) x[j][d] = valid ? src[(int64_t)d * N + gbase + e] : T(0);
-            id[j] = valid ? isrc[gbase + e] : 0;
+            id[j] = valid ? (isrc ? isrc[gbase + e] : (int32_t)(gbase + e)) : 0;  // level 0: ids = input rows
         }
 #pragma unroll
         for (int j = 0; j < CH; j++) {
@@ -1376,7 +1376,7 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
 
 template <typename T, int DT>
 __global__ void __launch_bounds__(32, 13)
-k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0, const int32_t* idx1, DevCtx c,
+k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, int32_t* idx0, const int32_t* idx1, DevCtx c,
           KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, SubStack* __restrict__ sstack,
           uint32_t* __restrict__ fyslots, int* __restrict__ fylocks, int32_t* task_nodes, int32_t* task_depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1385,8 +1385,9 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
     const int64_t N = c.N;
     const int ts = c.ts;
     const int lane = threadIdx.x & 31;
-    const T* src = tk.src ? buf1 : buf0;
-    const int32_t* isrc = tk.src ? idx1 : idx0;
+    // tk.src: 0 / 1 = build buffer, 2 = the caller's input (row ids = positions)
+    const T* src = tk.src == 2 ? in0 : (tk.src ? buf1 : buf0);
+    const int32_t* isrc = tk.src == 2 ? nullptr : (tk.src ? idx1 : idx0);
     KdNode* out_nodes = scratch + 2 * tk.start;
     int32_t* out_cnt = scnt + 2 * tk.start;
     SubStack* stk = sstack + 2 * tk.start;
@@ -1396,7 +1397,7 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
         if (tk.src) {
             for (int64_t e = lane; e < tk.n; e += 32) {
                 for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = src[(int64_t)d * N + tk.start + e];
-                idx0[tk.start + e] = isrc[tk.start + e];
+                idx0[tk.start + e] = isrc ? isrc[tk.start + e] : (int32_t)(tk.start + e);
             }
         }
         if (lane == 0) {
@@ -1509,7 +1510,7 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, int32_t* idx0,
 #pragma unroll
     for (int k2 = 0; k2 < MAXS / 32; k2++) {
         const int e = k2 * 32 + lane;
-        if (e < n) rid[k2] = isrc[tk.start + perm[0][e]];
+        if (e < n) rid[k2] = isrc ? isrc[tk.start + perm[0][e]] : (int32_t)(tk.start + perm[0][e]);
     }
     __syncwarp();
 #pragma unroll
@@ -1691,8 +1692,6 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
 
     T* buf[2] = {dalloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
     int32_t* idx[2] = {dalloc<int32_t>(n, st), dalloc<int32_t>(n, st)};
-    k_init<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_in, buf[0], idx[0], n, dims);
-    KD_CUDA(cudaGetLastError());
 
     // top store (grown per level)
     size_t ts_cap = 1024;
@@ -1740,7 +1739,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
             K = 1;
             tiles = (uint32_t)((n + TILE - 1) / TILE);
         } else {
-            Task t0{0, (int32_t)n, 0, 1ULL, 0, 0, 0, 0};
+            Task t0{0, (int32_t)n, 0, 1ULL, 0, 2, 0, 0};  // reads the input directly
             KD_CUDA(cudaMemcpyAsync(tasks, &t0, sizeof(Task), cudaMemcpyHostToDevice, st));
             const int one = 1;
             KD_CUDA(cudaMemcpyAsync(task_ctr, &one, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -1765,8 +1764,11 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
     int64_t max_node = n;  // largest node of the current level (read back with the level counters)
+    bool at_input = true;  // the first level reads the caller's points directly (row ids = positions)
     while (K > 0) {
         LNode* lv = levels.back();
+        const T* lsrc = at_input ? d_in : buf[par];
+        const int32_t* lidx = at_input ? nullptr : idx[par];
         const bool big_levels = max_node > (int64_t(1) << 22);
         // capacity: children slots and tasks
         if (ts_used + 2 * (size_t)K + 1 > ts_cap) {
@@ -1796,30 +1798,30 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
         KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
         if (K <= sample_cta_max) {
-            if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(buf[par], lv, c, split, wb, wf);
-            else k_sample_cta<T, 0><<<K, CTA_S, 0, st>>>(buf[par], lv, c, split, wb, wf);
+            if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
+            else k_sample_cta<T, 0><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
         } else {
             const unsigned sg = (unsigned)((K + SAMPLE_WARPS - 1) / SAMPLE_WARPS);
             if (dims == 3) {
-                k_sample<T, 3, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(buf[par], lv, K, c, split, wb, wf);
-                if (big_levels) k_sample<T, 3, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(buf[par], lv, K, c, split, wb, wf);
+                k_sample<T, 3, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(lsrc, lv, K, c, split, wb, wf);
+                if (big_levels) k_sample<T, 3, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(lsrc, lv, K, c, split, wb, wf);
             } else {
-                k_sample<T, 0, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(buf[par], lv, K, c, split, wb, wf);
-                if (big_levels) k_sample<T, 0, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(buf[par], lv, K, c, split, wb, wf);
+                k_sample<T, 0, false><<<sg, SAMPLE_WARPS * 32, sample_smem32, st>>>(lsrc, lv, K, c, split, wb, wf);
+                if (big_levels) k_sample<T, 0, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(lsrc, lv, K, c, split, wb, wf);
             }
         }
         int32_t* tmap = dalloc<int32_t>(tiles, st);
         k_tile_map<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tiles, tmap);
-        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, tmap, c, split, wb, wf);
+        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, wb, wf);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
-        k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(buf[par], lv, c, split, slow_list, slow_count);
-        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(buf[par], lv, tmap, c, split, tile_left);
+        k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
+        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, tile_left);
         size_t tmp_bytes = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
-    k_scatter<T, DTV, CHV><<<tiles, TILE_THREADS, 0, st>>>(buf[par], idx[par], buf[1 - par], idx[1 - par], lv, K, c, \
+    k_scatter<T, DTV, CHV><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, K, c, \
                                                            split, tile_loff)
         switch (dims) {
             case 1: KD_SCATTER(1, 16); break;
@@ -1831,7 +1833,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
 #undef KD_SCATTER
         LNode* next = dalloc<LNode>(2 * (size_t)K, st);
         KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long) + sizeof(int), st));
-        k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, par, (int)ts_used, ts, next, next_ctr,
+        k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, at_input ? 2 : par, (int)ts_used, ts, next, next_ctr,
                                                     tasks, task_ctr, reinterpret_cast<int*>(next_ctr + 1));
         KD_CUDA(cudaGetLastError());
         KD_CUDA(cudaMemcpyAsync(&h_ctr[0], next_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1851,6 +1853,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         tiles = (uint32_t)(h_ctr[0] & 0xFFFFFFFFULL);
         max_node = (int64_t)(int32_t)(h_ctr[2] & 0xFFFFFFFFULL);
         par = 1 - par;
+        at_input = false;
         if (K > 0) levels.push_back(next);
         else dfree(next, st);
     }
@@ -1868,11 +1871,11 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int* fylocks = reinterpret_cast<int*>(fyslots + (size_t)FY_SLOTS * 2 * MAXS);
     if (dims == 3) {
         KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
-        k_subtree<T, 3><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt, sstack,
+        k_subtree<T, 3><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
                                                       fyslots, fylocks, task_nodes, task_depth);
     } else {
         KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
-        k_subtree<T, 0><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], idx[0], idx[1], c, scratch, scnt, sstack,
+        k_subtree<T, 0><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
                                                       fyslots, fylocks, task_nodes, task_depth);
     }
     KD_CUDA(cudaGetLastError());
