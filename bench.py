@@ -119,6 +119,17 @@ def build_bytes(n, dims, leaf):
     return n * levels * (8 * dims + 12), levels
 
 
+def measured_traffic(config):
+    """ncu DRAM bytes (read + write) per build and per query batch, committed under
+    profiles/ by tools/traffic.py (C2 only; {} when absent)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"r01_traffic_{config.lower()}.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def query_bytes(dims, k, v, c):
     """B_q = 4D + 8V + 4D*C + 16k (V, C: reference counters)."""
     return 4 * dims + 8 * v + 4 * dims * c + 16 * k
@@ -353,7 +364,10 @@ def run_b200(args):
             v_ref, c_ref, ctr_src = 44.8, 156.3, "SURVEY §8(d) C2-like counters at 4M points"
         qb = query_bytes(w.dims, w.k, v_ref, c_ref)
         ach_q = q * qb / tq / 1e9
-        launches = levels * 9 + 5 + 2
+        # build: 10 launches per level + k_subtree, 2 per level preorder stitch, relocate, ids, leaf count;
+        # query: home-leaf keys, 5 CUB radix-sort kernels, k_knn_persist
+        launches = 12 * levels + 4 + 7
+        traffic = measured_traffic(args.config)
         line = {
             "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
             "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
@@ -366,12 +380,14 @@ def run_b200(args):
                        "parallelism": f"weak x{world}"},
             "ms_build": tb * 1e3, "ms_knn": tq * 1e3,
             "roofline": {"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s", "frac": ach_b / peak,
-                         "traffic": None, "kernel": "whole build (all build kernels of one kd_tree_build)",
+                         "traffic": traffic.get("build_dram_bytes"), "traffic_source": traffic.get("source"),
+                         "kernel": "whole build (all build kernels of one kd_tree_build)",
                          "algorithmic_bytes": bbytes, "model": f"N*L*(8D+12), L={levels_model}",
                          "peak_kind": peak_kind},
             "knn": {"value": world * q / tq, "unit": "queries/s",
                     "roofline": {"bound": "hbm", "achieved": ach_q, "peak": peak, "unit": "GB/s",
-                                 "frac": ach_q / peak, "traffic": None, "kernel": "k_knn",
+                                 "frac": ach_q / peak, "traffic": traffic.get("query_dram_bytes"),
+                                 "kernel": "query batch (home-leaf sort + k_knn_persist)",
                                  "bytes_per_query": qb, "model": "4D+8V+4DC+16k", "V": v_ref, "C": c_ref,
                                  "counters": ctr_src}},
             "sample_check_vs_fp64_bruteforce": ok,

@@ -40,6 +40,7 @@ constexpr int MAXS = 1024;       // max sample size supported on device
 constexpr int WIN = 256;         // histogram window (boundaries)
 constexpr int TILE = 4096;       // elements per tile CTA
 constexpr int TILE_THREADS = 256;
+constexpr int SUB = 2;  // partition sub-tiles per tile (k_count counts them, k_scatter moves one per CTA)
 constexpr int SAMPLE_WARPS = 4;
 constexpr int SLOW_THREADS = 256;
 constexpr double U64 = 1.1102230246251565e-16;  // 2^-53
@@ -841,12 +842,12 @@ __global__ void __launch_bounds__(TILE_THREADS)
 k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
         const Split* __restrict__ split, uint32_t* tile_left) {
     constexpr int EPT = TILE / TILE_THREADS;
-    __shared__ uint32_t red[TILE_THREADS / 32];
+    __shared__ uint32_t red[SUB][TILE_THREADS / 32];
     const uint32_t t = blockIdx.x;
     const int ni = tmap[t];
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
-    uint32_t cnt = 0;
+    uint32_t cnt[SUB] = {};
     if (sp.status == ST_SPLIT) {
         const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
         const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
@@ -860,16 +861,19 @@ k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_
 #pragma unroll
         for (int j = 0; j < EPT; j++) {
             const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-            cnt += (e < e1) && ((double)v[j] < sp.value);
+            cnt[j / (EPT / SUB)] += (e < e1) && ((double)v[j] < sp.value);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+#pragma unroll
+    for (int u = 0; u < SUB; u++) {
+        for (int o = 16; o > 0; o >>= 1) cnt[u] += __shfl_xor_sync(FULL, cnt[u], o);
+        if ((threadIdx.x & 31) == 0) red[u][threadIdx.x >> 5] = cnt[u];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < SUB) {
         uint32_t s = 0;
-        for (int w = 0; w < TILE_THREADS / 32; w++) s += red[w];
-        tile_left[t] = s;
+        for (int w = 0; w < TILE_THREADS / 32; w++) s += red[threadIdx.x][w];
+        tile_left[t * SUB + threadIdx.x] = s;
     }
 }
 
@@ -884,16 +888,17 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
     constexpr int DC = DT > 0 ? DT : 16;
     __shared__ uint32_t wl[CH * NW];
     __shared__ uint32_t wpre[CH * NW];
-    const uint32_t t = blockIdx.x;
+    const uint32_t t = blockIdx.x / SUB, sub = blockIdx.x % SUB;
     const int ni = tile_node(nodes, K, t);
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     if (sp.status != ST_SPLIT) return;
     const int D = DT > 0 ? DT : c.dims;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
-    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
-    const uint32_t lbefore = tile_loff[t] - tile_loff[nd.tile_off];  // lefts in earlier tiles of this node
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
+    if (e0 >= e1) return;
+    const uint32_t lbefore = tile_loff[blockIdx.x] - tile_loff[nd.tile_off * SUB];  // lefts earlier in this node
     int64_t lrun = lbefore;
     int64_t rrun = e0 - lbefore;
     const int64_t N = c.N;
@@ -1794,8 +1799,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         T* wb = dalloc<T>((size_t)K * WIN, st);
         uint32_t* wf = dalloc<uint32_t>((size_t)K * WIN, st);
         int* slow_list = dalloc<int>(K, st);
-        uint32_t* tile_left = dalloc<uint32_t>(tiles + 1, st);
-        uint32_t* tile_loff = dalloc<uint32_t>(tiles + 1, st);
+        uint32_t* tile_left = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
+        uint32_t* tile_loff = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
         KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
         if (K <= sample_cta_max) {
             if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
@@ -1817,16 +1822,16 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
         k_count<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, tile_left);
         size_t tmp_bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
-        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)tiles, st);
+        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
-    k_scatter<T, DTV, CHV><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, K, c, \
+    k_scatter<T, DTV, CHV><<<tiles * SUB, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, K, c, \
                                                            split, tile_loff)
         switch (dims) {
-            case 1: KD_SCATTER(1, 16); break;
-            case 2: KD_SCATTER(2, 16); break;
-            case 3: KD_SCATTER(3, 16); break;
+            case 1: KD_SCATTER(1, 8); break;
+            case 2: KD_SCATTER(2, 8); break;
+            case 3: KD_SCATTER(3, 8); break;
             case 4: KD_SCATTER(4, 8); break;
             default: KD_SCATTER(0, 2); break;
         }
