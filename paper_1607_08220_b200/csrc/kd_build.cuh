@@ -1,4 +1,5 @@
-// kd_build.cu -- reference-exact kd-tree construction on sm_100a.
+// kd_build.cuh -- reference-exact kd-tree construction on sm_100a (compiled once per
+// coordinate type by kd_build_f32.cu / kd_build_f64.cu).
 //
 // Reproduces kdknn.local_tree.build_local_tree (local_tree.py:436-574) byte for
 // byte: same split dimension (max sample variance, local_tree.py:111-146), same
@@ -40,7 +41,7 @@ constexpr int MAXS = 1024;       // max sample size supported on device
 constexpr int WIN = 256;         // histogram window (boundaries)
 constexpr int TILE = 4096;       // elements per tile CTA
 constexpr int TILE_THREADS = 256;
-constexpr int SUB = 2;  // partition sub-tiles per tile (k_count counts them, k_scatter moves one per CTA)
+constexpr int SUB = 2;  // partition half-tiles per tile (k_scatter moves one per CTA)
 constexpr int SAMPLE_WARPS = 4;
 constexpr int SLOW_THREADS = 256;
 constexpr double U64 = 1.1102230246251565e-16;  // 2^-53
@@ -122,16 +123,22 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     // get their own instantiation so the common one stays small
     if (BIG != (n > (1u << 22))) return;
     typedef typename std::conditional<BIG, uint64_t, uint32_t>::type FK;
-    FK* skeys = reinterpret_cast<FK*>(smem_raw) + warp * MAXS;
-    uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * MAXS * sizeof(FK)) + warp * MAXS;
-    uint16_t* gidx = reinterpret_cast<uint16_t*>(smem_raw + SAMPLE_WARPS * MAXS * (sizeof(FK) + 4)) + warp * MAXS;
+    // per warp: region 0 = FY sort keys (MAXS FK) or the direct table (FYD_MAX u16),
+    // then picked (MAXS u32), then gidx / back (MAXS u16)
+    constexpr size_t R0 = sizeof(FK) * MAXS > 2 * FYD_MAX ? sizeof(FK) * MAXS : 2 * FYD_MAX;
+    FK* skeys = reinterpret_cast<FK*>(smem_raw + warp * R0);
+    uint16_t* dlast = reinterpret_cast<uint16_t*>(skeys);
+    uint32_t* picked = reinterpret_cast<uint32_t*>(smem_raw + SAMPLE_WARPS * R0) + warp * MAXS;
+    uint16_t* gidx = reinterpret_cast<uint16_t*>(smem_raw + SAMPLE_WARPS * (R0 + 4 * MAXS)) + warp * MAXS;
+    const bool direct = !BIG && n <= (uint32_t)FYD_MAX;
     const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
 
     // --- variance sample (local_tree.py:122-132)
     const int take = (int)min((int64_t)n, c.vs);
     const uint64_t vseed = node_seed(c.seed, nd.path, 0);
-    fy_resolve<32, FK>(n, take, vseed, skeys, picked, gidx);
+    if (direct) fy_direct<32>(n, take, vseed, dlast, gidx, picked);
+    else fy_resolve<32, FK>(n, take, vseed, skeys, picked, gidx);
 
     int d0 = 0;
     double b0 = 0.0, e0 = 0.0;
@@ -142,21 +149,32 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
         eb[d] = 0.0;
         if (d >= D) continue;
         const T* row = src + (int64_t)d * N + nd.start;
+        // every gather of this dimension in flight at once; both passes read the registers
+        T xs[MAXS / 32];
+#pragma unroll
+        for (int r = 0; r < MAXS / 32; r++) {
+            const int j = r * 32 + lane;
+            xs[r] = j < take ? row[picked[j]] : T(0);
+        }
         double s1 = 0.0, sa = 0.0;
-#pragma unroll 4
-        for (int j = lane; j < take; j += 32) {
-            const double x = (double)row[picked[j]];
-            s1 = __dadd_rn(s1, x);
-            sa = __dadd_rn(sa, fabs(x));
+#pragma unroll
+        for (int r = 0; r < MAXS / 32; r++) {
+            if (r * 32 + lane < take) {
+                const double x = (double)xs[r];
+                s1 = __dadd_rn(s1, x);
+                sa = __dadd_rn(sa, fabs(x));
+            }
         }
         s1 = warp_sum(s1);
         sa = warp_sum(sa);
         const double mean = __ddiv_rn(s1, (double)take);
         double s2 = 0.0;
-#pragma unroll 4
-        for (int j = lane; j < take; j += 32) {
-            const double df = __dsub_rn((double)row[picked[j]], mean);
-            s2 = __dadd_rn(s2, __dmul_rn(df, df));
+#pragma unroll
+        for (int r = 0; r < MAXS / 32; r++) {
+            if (r * 32 + lane < take) {
+                const double df = __dsub_rn((double)xs[r], mean);
+                s2 = __dadd_rn(s2, __dmul_rn(df, df));
+            }
         }
         s2v[d] = warp_sum(s2);
         eb[d] = ssd_bound(s2v[d], sa, take);
@@ -193,7 +211,8 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const int m = (int)min((int64_t)n, c.ms);
     const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
     __syncwarp();
-    fy_resolve<32, FK>(n, m, mseed, skeys, picked, gidx);
+    if (direct) fy_direct<32>(n, m, mseed, dlast, gidx, picked);
+    else fy_resolve<32, FK>(n, m, mseed, skeys, picked, gidx);
     typedef typename KeyOf<T>::type Key;
     const T* row = src + (int64_t)d0 * N + nd.start;
     Key kv[32];
@@ -472,7 +491,7 @@ __device__ __forceinline__ int tile_node(const LNode* nodes, int K, uint32_t t) 
 }
 
 // tile -> node of the level (once per level, so the tile kernels start with one load)
-__global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32_t tiles, int32_t* __restrict__ tmap) {
+static __global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32_t tiles, int32_t* __restrict__ tmap) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < tiles) tmap[t] = tile_node(nodes, K, t);
 }
@@ -882,14 +901,14 @@ k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_
 template <typename T, int DT, int CH>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
-          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, int K, DevCtx c,
+          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
           const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff) {
     constexpr int NW = TILE_THREADS / 32;
     constexpr int DC = DT > 0 ? DT : 16;
     __shared__ uint32_t wl[CH * NW];
     __shared__ uint32_t wpre[CH * NW];
     const uint32_t t = blockIdx.x / SUB, sub = blockIdx.x % SUB;
-    const int ni = tile_node(nodes, K, t);
+    const int ni = tmap[t];
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     if (sp.status != ST_SPLIT) return;
@@ -989,7 +1008,7 @@ struct TopStore {
     int32_t* pre;    // preorder index
 };
 
-__global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* __restrict__ split, DevCtx c,
+static __global__ void k_children(const LNode* __restrict__ nodes, int K, const Split* __restrict__ split, DevCtx c,
                            int dst_parity, int src_parity, int child_base, TopStore ts, LNode* next,
                            unsigned long long* next_ctr, Task* tasks, int* task_ctr, int* next_max) {
     const int ni = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1139,7 +1158,7 @@ __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, in
     nxt = nx;
 }
 
-__device__ __noinline__ void fy_resolve_n(uint32_t n, uint64_t seed, uint32_t* fk, uint32_t* fp) {
+static __device__ __noinline__ void fy_resolve_n(uint32_t n, uint64_t seed, uint32_t* fk, uint32_t* fp) {
     if (n <= 32) fy_resolve<1, uint32_t>(n, (int)n, seed, fk, fp);
     else if (n <= 64) fy_resolve<2, uint32_t>(n, (int)n, seed, fk, fp);
     else if (n <= 128) fy_resolve<4, uint32_t>(n, (int)n, seed, fk, fp);
@@ -1536,7 +1555,7 @@ __device__ __forceinline__ int child_nodes(const TopStore& ts, const int32_t* ta
     return ts.kind[s] == TS_TASK ? task_nodes[ts.task[s]] : ts.nodes[s];
 }
 
-__global__ void k_top_count(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes) {
+static __global__ void k_top_count(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= K) return;
     const int s = lv[i].slot;
@@ -1544,7 +1563,7 @@ __global__ void k_top_count(const LNode* lv, int K, TopStore ts, const int32_t* 
     ts.nodes[s] = 1 + child_nodes(ts, task_nodes, ts.left[s]) + child_nodes(ts, task_nodes, ts.right[s]);
 }
 
-__global__ void k_top_pre(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes, int32_t* task_base,
+static __global__ void k_top_pre(const LNode* lv, int K, TopStore ts, const int32_t* task_nodes, int32_t* task_base,
                           KdNode* nodes, int32_t* ncount) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= K) return;
@@ -1561,7 +1580,7 @@ __global__ void k_top_pre(const LNode* lv, int K, TopStore ts, const int32_t* ta
     ncount[p] = ts.npts[s];
 }
 
-__global__ void k_relocate(const Task* tasks, const int32_t* task_nodes, const int32_t* task_base,
+static __global__ void k_relocate(const Task* tasks, const int32_t* task_nodes, const int32_t* task_base,
                            const KdNode* scratch, const int32_t* scnt, KdNode* nodes, int32_t* ncount) {
     const Task tk = tasks[blockIdx.x];
     const int cnt = task_nodes[blockIdx.x];
@@ -1576,7 +1595,7 @@ __global__ void k_relocate(const Task* tasks, const int32_t* task_nodes, const i
     }
 }
 
-__global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const int32_t* __restrict__ perm,
+static __global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const int32_t* __restrict__ perm,
                              uint64_t* __restrict__ ids_out, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) ids_out[i] = ids_in ? ids_in[perm[i]] : (uint64_t)perm[i];
@@ -1590,7 +1609,7 @@ __global__ void k_init(const T* __restrict__ in, T* __restrict__ buf, int32_t* _
     idx[i] = (int32_t)i;
 }
 
-__global__ void k_count_leaves(const KdNode* nodes, int64_t nn, unsigned long long* out) {
+static __global__ void k_count_leaves(const KdNode* nodes, int64_t nn, unsigned long long* out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool leaf = i < nn && nodes[i].db < 0;
     const unsigned b = __ballot_sync(FULL, leaf);
@@ -1621,10 +1640,12 @@ static unsigned long long* pinned_counters(int) {
     return p;
 }
 
+uint32_t* fy_slots(int device, cudaStream_t st);  // persistent per-device scratch (kd_build_f32.cu)
+#ifdef KD_BUILD_COMMON
 static std::mutex g_init_mu;
 
 // persistent per-device scratch for the rare exact-variance path of k_subtree
-static uint32_t* fy_slots(int device, cudaStream_t st) {
+uint32_t* fy_slots(int device, cudaStream_t st) {
     static uint32_t* slots[64] = {nullptr};
     std::lock_guard<std::mutex> lk(g_init_mu);
     if (!slots[device]) {
@@ -1646,6 +1667,8 @@ void retain_pool(int device) {
     }
     done[device] = true;
 }
+
+#endif
 
 struct HostTrace {
     bool on = std::getenv("KDB_TRACE") != nullptr;
@@ -1755,8 +1778,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int ntasks_known = K == 0 ? 1 : 0;
     {
     }
-    const size_t sample_smem32 = (size_t)SAMPLE_WARPS * MAXS * (4 + 4 + 2);
-    const size_t sample_smem64 = (size_t)SAMPLE_WARPS * MAXS * (8 + 4 + 2);
+    const size_t sample_smem32 = (size_t)SAMPLE_WARPS * (std::max<size_t>(4 * MAXS, 2 * FYD_MAX) + MAXS * (4 + 2));
+    const size_t sample_smem64 = (size_t)SAMPLE_WARPS * (std::max<size_t>(8 * MAXS, 2 * FYD_MAX) + MAXS * (4 + 2));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem32));
     KD_CUDA(cudaFuncSetAttribute(k_sample<T, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sample_smem64));
@@ -1826,7 +1849,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
-    k_scatter<T, DTV, CHV><<<tiles * SUB, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, K, c, \
+    k_scatter<T, DTV, CHV><<<tiles * SUB, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, tmap, c, \
                                                            split, tile_loff)
         switch (dims) {
             case 1: KD_SCATTER(1, 8); break;
@@ -1948,15 +1971,13 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     tr.mark("exit");
 }
 
+#ifdef KD_BUILD_COMMON
 void free_tree(KdTreeDev* t) {
     if (!t) return;
     cudaFree(t->nodes); cudaFree(t->node_count); cudaFree(t->coords); cudaFree(t->ids); cudaFree(t->perm);
     t->nodes = nullptr; t->node_count = nullptr; t->coords = nullptr; t->ids = nullptr; t->perm = nullptr;
 }
 
-template void build_tree<float>(const float*, const uint64_t*, int64_t, int, const BuildCfg&, cudaStream_t, KdTreeDev*,
-                                BuildStats*);
-template void build_tree<double>(const double*, const uint64_t*, int64_t, int, const BuildCfg&, cudaStream_t,
-                                 KdTreeDev*, BuildStats*);
+#endif
 
 }  // namespace kdb

@@ -1,6 +1,7 @@
 // kd_capi.cu -- extern "C" boundary (include/kdtree_b200.h) over the device build/query.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -323,32 +324,6 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.sort_queries = !(flags & KD_NO_SORT);
         a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
         DevBuf bq, br, be, bd, bi, bc, bctr;
-        if (dev_ptrs) {
-            a.queries = queries; a.radii = radii; a.excl = exclude_ids;
-            a.out_d = out_d; a.out_i = out_i; a.out_c = out_c; a.out_ctr = out_ctr;
-        } else {
-            new (&bq) DevBuf(nq * D * 8, st);
-            KD_CUDA(cudaMemcpyAsync(bq.p, queries, nq * D * 8, cudaMemcpyHostToDevice, st));
-            a.queries = (const double*)bq.p;
-            if (radii) {
-                new (&br) DevBuf(nq * 8, st);
-                KD_CUDA(cudaMemcpyAsync(br.p, radii, nq * 8, cudaMemcpyHostToDevice, st));
-                a.radii = (const double*)br.p;
-            }
-            if (exclude_ids) {
-                new (&be) DevBuf(nq * 8, st);
-                KD_CUDA(cudaMemcpyAsync(be.p, exclude_ids, nq * 8, cudaMemcpyHostToDevice, st));
-                a.excl = (const uint64_t*)be.p;
-            }
-            new (&bd) DevBuf(nq * k * 8, st);
-            new (&bi) DevBuf(nq * k * 8, st);
-            new (&bc) DevBuf(nq * 8, st);
-            a.out_d = (double*)bd.p; a.out_i = (uint64_t*)bi.p; a.out_c = (int64_t*)bc.p;
-            if (out_ctr) {
-                new (&bctr) DevBuf(nq * 3 * 8, st);
-                a.out_ctr = (int64_t*)bctr.p;
-            }
-        }
         DevBuf hd, hi;
         if (k > 32) {
             new (&hd) DevBuf(nq * k * 8, st);
@@ -356,14 +331,67 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
             a.heap_d = (double*)hd.p;
             a.heap_i = (uint64_t*)hi.p;
         }
-        knn(d, a, st);
-        if (!dev_ptrs) {
-            KD_CUDA(cudaMemcpyAsync(out_d, a.out_d, nq * k * 8, cudaMemcpyDeviceToHost, st));
-            KD_CUDA(cudaMemcpyAsync(out_i, a.out_i, nq * k * 8, cudaMemcpyDeviceToHost, st));
-            KD_CUDA(cudaMemcpyAsync(out_c, a.out_c, nq * 8, cudaMemcpyDeviceToHost, st));
-            if (out_ctr) KD_CUDA(cudaMemcpyAsync(out_ctr, a.out_ctr, nq * 3 * 8, cudaMemcpyDeviceToHost, st));
-            KD_CUDA(cudaStreamSynchronize(st));
+        if (dev_ptrs) {
+            a.queries = queries; a.radii = radii; a.excl = exclude_ids;
+            a.out_d = out_d; a.out_i = out_i; a.out_c = out_c; a.out_ctr = out_ctr;
+            knn(d, a, st);
+            return KD_OK;
         }
+        // host buffers: device staging for the whole batch, then a pipeline over
+        // query chunks -- H2D of chunk c+1 and D2H of chunk c-1 (copy engines, one
+        // per direction) overlap the search of chunk c on the caller's stream
+        new (&bq) DevBuf(nq * D * 8, st);
+        if (radii) new (&br) DevBuf(nq * 8, st);
+        if (exclude_ids) new (&be) DevBuf(nq * 8, st);
+        new (&bd) DevBuf(nq * k * 8, st);
+        new (&bi) DevBuf(nq * k * 8, st);
+        new (&bc) DevBuf(nq * 8, st);
+        if (out_ctr) new (&bctr) DevBuf(nq * 3 * 8, st);
+        const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(KNN_MAX_CHUNKS, nq / KNN_CHUNK_MIN));
+        const int64_t csz = (nq + nch - 1) / nch;
+        cudaStream_t s_in = nullptr, s_out = nullptr;
+        KD_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+        KD_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+        std::vector<cudaEvent_t> evs(2 * nch + 2, nullptr);
+        for (auto& e : evs) KD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        KD_CUDA(cudaEventRecord(evs[2 * nch], st));  // staging allocated
+        KD_CUDA(cudaStreamWaitEvent(s_in, evs[2 * nch], 0));
+        KD_CUDA(cudaStreamWaitEvent(s_out, evs[2 * nch], 0));
+        for (int64_t c = 0; c < nch; c++) {
+            const int64_t lo = c * csz, cnt = std::min(csz, nq - lo);
+            if (cnt <= 0) break;
+            KD_CUDA(cudaMemcpyAsync((double*)bq.p + lo * D, queries + lo * D, cnt * D * 8, cudaMemcpyHostToDevice, s_in));
+            if (radii) KD_CUDA(cudaMemcpyAsync((double*)br.p + lo, radii + lo, cnt * 8, cudaMemcpyHostToDevice, s_in));
+            if (exclude_ids)
+                KD_CUDA(cudaMemcpyAsync((uint64_t*)be.p + lo, exclude_ids + lo, cnt * 8, cudaMemcpyHostToDevice, s_in));
+            KD_CUDA(cudaEventRecord(evs[2 * c], s_in));
+            KD_CUDA(cudaStreamWaitEvent(st, evs[2 * c], 0));
+            KnnArgs ac = a;
+            ac.nq = cnt;
+            ac.queries = (const double*)bq.p + lo * D;
+            ac.radii = radii ? (const double*)br.p + lo : nullptr;
+            ac.excl = exclude_ids ? (const uint64_t*)be.p + lo : nullptr;
+            ac.out_d = (double*)bd.p + lo * k;
+            ac.out_i = (uint64_t*)bi.p + lo * k;
+            ac.out_c = (int64_t*)bc.p + lo;
+            ac.out_ctr = out_ctr ? (int64_t*)bctr.p + lo * 3 : nullptr;
+            if (k > 32) { ac.heap_d = a.heap_d + lo * k; ac.heap_i = a.heap_i + lo * k; }
+            knn(d, ac, st);
+            KD_CUDA(cudaEventRecord(evs[2 * c + 1], st));
+            KD_CUDA(cudaStreamWaitEvent(s_out, evs[2 * c + 1], 0));
+            KD_CUDA(cudaMemcpyAsync(out_d + lo * k, ac.out_d, cnt * k * 8, cudaMemcpyDeviceToHost, s_out));
+            KD_CUDA(cudaMemcpyAsync(out_i + lo * k, ac.out_i, cnt * k * 8, cudaMemcpyDeviceToHost, s_out));
+            KD_CUDA(cudaMemcpyAsync(out_c + lo, ac.out_c, cnt * 8, cudaMemcpyDeviceToHost, s_out));
+            if (out_ctr) KD_CUDA(cudaMemcpyAsync(out_ctr + lo * 3, ac.out_ctr, cnt * 3 * 8, cudaMemcpyDeviceToHost, s_out));
+        }
+        // the caller's stream (and the staging frees queued on it) follows the last copy-out
+        KD_CUDA(cudaEventRecord(evs[2 * nch + 1], s_out));
+        KD_CUDA(cudaStreamWaitEvent(st, evs[2 * nch + 1], 0));
+        KD_CUDA(cudaStreamSynchronize(s_out));
+        KD_CUDA(cudaStreamSynchronize(st));
+        for (auto& e : evs) cudaEventDestroy(e);
+        cudaStreamDestroy(s_in);
+        cudaStreamDestroy(s_out);
     });
     return KD_OK;
 }

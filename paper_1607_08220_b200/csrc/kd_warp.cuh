@@ -215,4 +215,63 @@ __device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t*
     __syncwarp();
 }
 
+// Partial Fisher-Yates for nodes of at most FYD_MAX points, without sorting.
+// Same draws as fy_resolve (median.py:74-85).  Step j targets r_j in [j, n);
+// the value drawn is the one at slot r_j before step j.  A slot s >= j is only
+// ever written by earlier steps that targeted it, so with
+//   prev(j) = latest step i < j with r_i = r_j        (none -> slot untouched)
+//   back(t) = latest step i < t with r_i = t, t < m   (none -> slot t untouched)
+//   W(i)    = value at slot i before step i = back(i) ? W(back(i)) : i
+// the draw is picked[j] = prev(j) ? W(prev(j)) : r_j.  prev() comes from 32
+// rounds of 32 steps against a direct table last[slot] (latest step so far),
+// with same-round collisions resolved by __match_any_sync; back(t) is prev(t)
+// when step t targeted itself, else the final last[t] (no step after t can
+// target t).  Shared scratch: last[n] u16, back[m] u16, picked[m] u32.
+constexpr int FYD_MAX = 4096;
+constexpr uint16_t FYD_NONE = 0xFFFF;
+
+template <int R>
+__device__ void fy_direct(uint32_t n, int m, uint64_t seed, uint16_t* last, uint16_t* back, uint32_t* picked) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    for (uint32_t i = lane; i < (n + 1) / 2; i += 32) reinterpret_cast<uint32_t*>(last)[i] = 0xFFFFFFFFu;
+    __syncwarp();
+#pragma unroll 1
+    for (int r = 0; r < R; r++) {
+        const int j = r * 32 + lane;
+        const bool act = j < m;
+        uint32_t tgt = 0xFFFFFFFFu;
+        if (act) {
+            const uint64_t z = rng_at(seed, (uint64_t)j);
+            tgt = (uint32_t)j + (uint32_t)mod_u64_u32(z, n - (uint32_t)j);
+        }
+        const unsigned grp = __match_any_sync(FULL, tgt);
+        const unsigned lower = grp & lt;
+        uint32_t pv = FYD_NONE;
+        if (act) pv = lower ? (uint32_t)(r * 32 + 31 - __clz(lower)) : (uint32_t)last[tgt];
+        __syncwarp();
+        // the highest lane of each target group records the latest step
+        if (act && (grp >> lane) == 1u) last[tgt] = (uint16_t)j;
+        if (act) picked[j] = tgt | (pv << 16);
+        __syncwarp();
+    }
+    for (int j = lane; j < m; j += 32) {
+        const uint32_t w = picked[j];
+        const uint32_t tgt = w & 0xFFFFu;
+        back[j] = tgt == (uint32_t)j ? (uint16_t)(w >> 16) : last[j];
+    }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) {
+        const uint32_t w = picked[j];
+        uint32_t i = w >> 16;
+        uint32_t val = w & 0xFFFFu;
+        if (i != FYD_NONE) {
+            while (back[i] != FYD_NONE) i = back[i];
+            val = i;
+        }
+        picked[j] = val;
+    }
+    __syncwarp();
+}
+
 }  // namespace kdb
