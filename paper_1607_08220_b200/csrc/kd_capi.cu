@@ -325,7 +325,7 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
         DevBuf bq, br, be, bd, bi, bc, bctr;
         DevBuf hd, hi;
-        if (k > 32) {
+        if (k > 32 || (k == 32 && exclude_ids && !a.thread_per_query)) {  // heap kernel scratch
             new (&hd) DevBuf(nq * k * 8, st);
             new (&hi) DevBuf(nq * k * 8, st);
             a.heap_d = (double*)hd.p;
@@ -375,7 +375,7 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
             ac.out_i = (uint64_t*)bi.p + lo * k;
             ac.out_c = (int64_t*)bc.p + lo;
             ac.out_ctr = out_ctr ? (int64_t*)bctr.p + lo * 3 : nullptr;
-            if (k > 32) { ac.heap_d = a.heap_d + lo * k; ac.heap_i = a.heap_i + lo * k; }
+            if (a.heap_d) { ac.heap_d = a.heap_d + lo * k; ac.heap_i = a.heap_i + lo * k; }
             knn(d, ac, st);
             KD_CUDA(cudaEventRecord(evs[2 * c + 1], st));
             KD_CUDA(cudaStreamWaitEvent(s_out, evs[2 * c + 1], 0));

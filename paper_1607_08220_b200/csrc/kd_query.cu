@@ -319,8 +319,9 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
 // imbalance of one-query-per-thread warps (a warp otherwise waits for its
 // slowest query) while keeping neighbouring lanes on neighbouring queries.
 // ----------------------------------------------------------------------------
+// low-dimensional, small-k instances are held to 72 registers (7 CTAs of 4 warps per SM)
 template <typename T, int DT, int KM>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, (DT > 0 && DT <= 3 && KM <= 8) ? 7 : 1)
 k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
               const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
               const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
@@ -337,6 +338,9 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     double radius = 0.0;
     uint64_t ex = ~0ULL;
     const bool has_ex = excl != nullptr;
+    // with an excluded id the search keeps k+1 candidates and drops that id at
+    // output: top-(k+1) minus {ex}, truncated to k == top-k of the set minus {ex}
+    const int kk = k + (has_ex ? 1 : 0);
     int64_t qi = -1;
     int64_t c0 = 0, c1 = 0, c2 = 0;
     double bd[KM];
@@ -357,7 +361,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
 
     auto admissible = [&](float b) {
         const double bb = (double)b;
-        return cnt < k ? bb < radius : bb <= kth_d;
+        return cnt < kk ? bb < radius : bb <= kth_d;
     };
     // exact fp32 pre-filter for float trees: a point whose binary64 distance d
     // can still be admitted (d <= R, R = radius or k-th distance) has an fp32
@@ -448,55 +452,17 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
             continue;
         }
         if (node < 0) continue;
-        // ---- descend to a leaf, pushing admissible far children
+        // ---- descend to a leaf, pushing admissible far children (node steps only;
+        // the bucket is scanned below, after the warp reconverges, so every lane
+        // that reached a leaf in this round scans at the same time)
+        int lstart = 0, llen = 0;
         for (;;) {
             c0++;
             const KdNode rec = nodes[node];
             if (rec.db < 0 && node == home) break;  // already scanned by the first descent
             if (rec.db < 0) {
-                // ---- scan the bucket
-                const int start = rec.a, len = -1 - rec.db;
-                c1++;
-                c2 += len;
-                for (int i = start; i < start + len; i++) {
-                    T cv[DC];
-#pragma unroll
-                    for (int d = 0; d < DC; d++)
-                        if (d < D) cv[d] = coords[(int64_t)d * n + i];
-                    if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
-                        float d32 = 0.0f;
-#pragma unroll
-                        for (int d = 0; d < DC; d++) {
-                            if (d < D) {
-                                const float tt = cv[d] - q32[d];
-                                d32 = fmaf(tt, tt, d32);
-                            }
-                        }
-                        if (d32 > thr32) continue;
-                    }
-                    double dist = 0.0;
-#pragma unroll
-                    for (int d = 0; d < DC; d++) {
-                        if (d < D) {
-                            const double df = __dsub_rn((double)cv[d], q[d]);
-                            dist = __dadd_rn(dist, __dmul_rn(df, df));
-                        }
-                    }
-                    if (cnt < k) {
-                        if (!(dist < radius)) continue;
-                    } else if (!(dist <= kth_d)) {
-                        continue;
-                    }
-                    if (has_ex && ids[i] == ex) continue;
-                    if (cnt == k && !lexless_pos(dist, (uint32_t)i, kth_d, kth_p, ids)) continue;
-                    topk_insert_pos<KM>(bd, bp, cnt, k, dist, (uint32_t)i, ids);
-                    if (cnt == k) {
-#pragma unroll
-                        for (int j = 0; j < KM; j++)
-                            if (j == k - 1) { kth_d = bd[j]; kth_p = bp[j]; }
-                        if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) thr32 = make_thr(kth_d);
-                    }
-                }
+                lstart = rec.a;
+                llen = -1 - rec.db;
                 break;
             }
             const int dim = rec.db;
@@ -522,6 +488,59 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 sp++;
             }
             node = near;
+        }
+        // ---- scan the bucket
+        if (llen > 0) {
+            const int start = lstart, len = llen;
+            c1++;
+            c2 += len;
+            // software-pipelined: the next point's coordinates are in flight
+            // while this one is evaluated
+            T cv[DC], nv[DC];
+#pragma unroll
+            for (int d = 0; d < DC; d++)
+                if (d < D) cv[d] = coords[(int64_t)d * n + start];
+            for (int i = start; i < start + len; i++) {
+                if (i + 1 < start + len) {
+#pragma unroll
+                    for (int d = 0; d < DC; d++)
+                        if (d < D) nv[d] = coords[(int64_t)d * n + i + 1];
+                }
+                bool take = true;
+                if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
+                    float d32 = 0.0f;
+#pragma unroll
+                    for (int d = 0; d < DC; d++) {
+                        if (d < D) {
+                            const float tt = cv[d] - q32[d];
+                            d32 = fmaf(tt, tt, d32);
+                        }
+                    }
+                    take = !(d32 > thr32);
+                }
+                if (take) {
+                    double dist = 0.0;
+#pragma unroll
+                    for (int d = 0; d < DC; d++) {
+                        if (d < D) {
+                            const double df = __dsub_rn((double)cv[d], q[d]);
+                            dist = __dadd_rn(dist, __dmul_rn(df, df));
+                        }
+                    }
+                    if (cnt < kk ? dist < radius
+                                 : (dist <= kth_d && lexless_pos(dist, (uint32_t)i, kth_d, kth_p, ids))) {
+                        topk_insert_pos<KM>(bd, bp, cnt, kk, dist, (uint32_t)i, ids);
+                        if (cnt == kk) {
+#pragma unroll
+                            for (int j = 0; j < KM; j++)
+                                if (j == kk - 1) { kth_d = bd[j]; kth_p = bp[j]; }
+                            if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) thr32 = make_thr(kth_d);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int d = 0; d < DC; d++) cv[d] = nv[d];
+            }
         }
         // ---- after the home leaf: restart from the root with a real k-th distance
         if (first) {
@@ -552,14 +571,22 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
             c0++;
         }
         if (node < 0) {
-            out_c[qi] = cnt;
+            int w = 0;
+            bool dropped = false;
 #pragma unroll
             for (int j = 0; j < KM; j++) {
                 if (j < cnt) {
-                    out_d[qi * (int64_t)k + j] = bd[j];
-                    out_i[qi * (int64_t)k + j] = ids[bp[j]];
+                    const uint64_t id = ids[bp[j]];
+                    if (has_ex && !dropped && id == ex) {
+                        dropped = true;
+                    } else if (w < k) {
+                        out_d[qi * (int64_t)k + w] = bd[j];
+                        out_i[qi * (int64_t)k + w] = id;
+                        w++;
+                    }
                 }
             }
+            out_c[qi] = w;
             if (out_ctr) {
                 out_ctr[qi * 3 + 0] = c0;
                 out_ctr[qi * 3 + 1] = c1;
@@ -653,14 +680,18 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
 template <typename T, int DT>
 static void dispatch_k(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, const uint32_t* home,
                        cudaStream_t st) {
-    if (a.k == 1) launch_knn<T, DT, 1>(t, a, order, home, st);
-    else if (a.k == 2) launch_knn<T, DT, 2>(t, a, order, home, st);
-    else if (a.k <= 4) launch_knn<T, DT, 4>(t, a, order, home, st);
-    else if (a.k == 5) launch_knn<T, DT, 5>(t, a, order, home, st);
-    else if (a.k == 6) launch_knn<T, DT, 6>(t, a, order, home, st);
-    else if (a.k <= 8) launch_knn<T, DT, 8>(t, a, order, home, st);
-    else if (a.k <= 16) launch_knn<T, DT, 16>(t, a, order, home, st);
-    else if (a.k <= 32) launch_knn<T, DT, 32>(t, a, order, home, st);
+    // list capacity: k, or k+1 when the persistent kernel carries an excluded id
+    // (k = 32 with an excluded id falls through to the heap kernel)
+    const int64_t kc = a.k + ((a.excl && !a.thread_per_query) ? 1 : 0);
+    if (kc == 1) launch_knn<T, DT, 1>(t, a, order, home, st);
+    else if (kc == 2) launch_knn<T, DT, 2>(t, a, order, home, st);
+    else if (kc <= 4) launch_knn<T, DT, 4>(t, a, order, home, st);
+    else if (kc == 5) launch_knn<T, DT, 5>(t, a, order, home, st);
+    else if (kc == 6) launch_knn<T, DT, 6>(t, a, order, home, st);
+    else if (kc <= 8) launch_knn<T, DT, 8>(t, a, order, home, st);
+    else if (kc <= 11) launch_knn<T, DT, 11>(t, a, order, home, st);
+    else if (kc <= 16) launch_knn<T, DT, 16>(t, a, order, home, st);
+    else if (kc <= 32) launch_knn<T, DT, 32>(t, a, order, home, st);
     else launch_knn<T, DT, 0>(t, a, order, home, st);
 }
 

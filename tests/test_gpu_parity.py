@@ -188,6 +188,30 @@ def test_self_exclusion_matches_k_plus_one(api, oracle):
         assert np.array_equal(i[r], bi[r, :bc[r]][keep][:5])
 
 
+@pytest.mark.parametrize("k,dims,kind", [(1, 3, "halo-f32"), (5, 3, "duplicate-heavy"), (10, 10, "f32"), (31, 3, "f32"),
+                                          (32, 3, "halo-f32"), (40, 2, "f32")])
+def test_exclusion_any_id_matches_oracle(api, oracle, k, dims, kind):
+    """exclude_ids with self ids, ids of other points and ids absent from the tree:
+    every row equals the brute-force top-k of the point set minus that id."""
+    core, lt, lq = api
+    rows = make_rows(20_000, dims, 31 + k, kind)
+    ps = core.PointSet.from_rows(rows)
+    tree = lt.build_local_tree(ps, lt.BuildConfig(bucket_size=16))
+    rng = np.random.default_rng(k)
+    sel = rng.choice(20_000, 1500, replace=False)
+    q = rows[sel]
+    ex = ps.ids[sel].copy()
+    ex[::3] = ps.ids[rng.choice(20_000, len(ex[::3]))]   # some other point's id
+    ex[1::7] = np.uint64(10**12)                          # an id not in the tree
+    d, i, c, _ = lq.find_knn_batch(tree, q, k, exclude_ids=ex)
+    bd, bi, bc = oracle.brute_knn(ps.coords, ps.ids, q, k + 1)
+    for r in range(len(sel)):
+        keep = bi[r, :bc[r]] != ex[r]
+        wd, wi = bd[r, :bc[r]][keep][:k], bi[r, :bc[r]][keep][:k]
+        assert c[r] == len(wd)
+        assert np.array_equal(d[r, :c[r]], wd) and np.array_equal(i[r, :c[r]], wi)
+
+
 def test_large_uniform_tree_and_sampled_knn(api, oracle):
     core, lt, lq = api
     rows = make_rows(2_000_000, 3, 21, "f32")
