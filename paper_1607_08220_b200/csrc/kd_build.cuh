@@ -18,7 +18,8 @@
 //     k_select   warp/node  exact binary64 median selection from the window
 //     k_slow     CTA/node   exact slow path (full histogram, exact fallback,
 //                           next dimensions) -- only for flagged nodes
-//     k_count/scan/k_scatter  stable segmented partition of coords + row ids
+//     k_tile_left/scan/k_scatter  stable segmented partition of coords + row ids
+//                           (per-half-tile left counts from k_hist's window rows)
 //     k_children thread/node child records, next level, subtree tasks
 //   then one CTA per subtree of <= min(1024, samples) points, built entirely in
 //   shared memory (k_subtree), and a preorder stitch (k_top_* / k_relocate).
@@ -64,7 +65,7 @@ struct Split {
     int32_t nb;
     int32_t wlo;
     int32_t whi;
-    int32_t pad;
+    int32_t wsel;  // window index of the chosen split value (k_select), -1 when the slow path chose it
     double value;
     int64_t nl;
     unsigned long long L;
@@ -498,18 +499,23 @@ static __global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32
 
 // ============================================================================
 // k_hist: windowed histogram (median.py:128-140 restricted to the boundaries
-// around the sampled median; counts below the window are aggregated in L)
+// around the sampled median; counts below the window are aggregated in L).
+// Besides the node totals it records, per half-tile, the window histogram row
+// and the below-window count: once k_select has chosen the split boundary,
+// each half-tile's "left" count is L_h + sum(row_h[1..wsel]) (k_tile_left), so
+// the partition needs no second pass over the split column.
 // ============================================================================
 template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c, Split* split,
-       const T* __restrict__ wb, uint32_t* __restrict__ wf) {
+       const T* __restrict__ wb, uint32_t* __restrict__ wf, uint16_t* __restrict__ hrow, uint32_t* __restrict__ hL) {
     constexpr int EPT = TILE / TILE_THREADS;
+    constexpr int HPT = EPT / SUB;  // elements per thread in each half-tile
     constexpr int NW = TILE_THREADS / 32;
     __shared__ T sb[WIN];
-    __shared__ uint32_t sf[WIN];
+    __shared__ uint32_t sf[SUB][WIN];
     __shared__ T q[NW][64];  // per-warp queue of in-window values (keeps the searches warp-dense)
-    __shared__ unsigned long long sL;
+    __shared__ uint32_t sL[SUB];
     const uint32_t t = blockIdx.x;
     const int ni = tmap[t];
     const LNode nd = nodes[ni];
@@ -528,46 +534,88 @@ k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t
     }
     // sb[i] = boundary i+1 for i < nw-2, +inf above: bin of x = 1 + #{i : sb[i] <= x}
     for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
-        sf[i] = 0;
+        sf[0][i] = 0;
+        sf[1][i] = 0;
         sb[i] = i < nw - 2 ? wb[(int64_t)ni * WIN + i + 1] : T(INFINITY);
     }
-    if (threadIdx.x == 0) sL = 0;
+    if (threadIdx.x < SUB) sL[threadIdx.x] = 0;
     const T lo_b = wb[(int64_t)ni * WIN], hi_b = wb[(int64_t)ni * WIN + nw - 1];
     __syncthreads();
-    auto search = [&](T x) {  // branchless upper_bound of x in the boundaries 1 .. nw-2
-        int pos = 0;
 #pragma unroll
-        for (int step = WIN / 2; step > 0; step >>= 1)
-            if (sb[pos + step - 1] <= x) pos += step;
-        atomicAdd(&sf[1 + pos], 1u);
-    };
-    uint32_t lc = 0;
-    int qn = 0;  // warp-uniform queue length
+    for (int h = 0; h < SUB; h++) {
+        uint32_t* hist = sf[h];
+        auto search = [&](T x) {  // branchless upper_bound of x in the boundaries 1 .. nw-2
+            int pos = 0;
 #pragma unroll
-    for (int j = 0; j < EPT; j++) {
-        const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-        const bool ok = e < e1;
-        const bool below = ok && v[j] < lo_b;
-        const bool inwin = ok && !below && v[j] < hi_b;
-        lc += below;
-        const unsigned m = __ballot_sync(FULL, inwin);
-        if (inwin) q[warp][qn + __popc(m & ((1u << lane) - 1))] = v[j];
-        qn += __popc(m);
-        if (qn >= 32) {  // one dense round of 32 searches
-            __syncwarp();
-            search(q[warp][qn - 32 + lane]);
-            qn -= 32;
-            __syncwarp();
+            for (int step = WIN / 2; step > 0; step >>= 1)
+                if (sb[pos + step - 1] <= x) pos += step;
+            atomicAdd(&hist[1 + pos], 1u);
+        };
+        uint32_t lc = 0;
+        int qn = 0;  // warp-uniform queue length
+#pragma unroll
+        for (int jj = 0; jj < HPT; jj++) {
+            const int j = h * HPT + jj;
+            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
+            const bool ok = e < e1;
+            const bool below = ok && v[j] < lo_b;
+            const bool inwin = ok && !below && v[j] < hi_b;
+            lc += below;
+            const unsigned m = __ballot_sync(FULL, inwin);
+            if (inwin) q[warp][qn + __popc(m & ((1u << lane) - 1))] = v[j];
+            qn += __popc(m);
+            if (qn >= 32) {  // one dense round of 32 searches
+                __syncwarp();
+                search(q[warp][qn - 32 + lane]);
+                qn -= 32;
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        if (lane < qn) search(q[warp][lane]);
+        __syncwarp();
+        for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
+        if (lane == 0 && lc) atomicAdd(&sL[h], lc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (sL[0] + sL[1])) atomicAdd(&split[ni].L, (unsigned long long)(sL[0] + sL[1]));
+    if (threadIdx.x < SUB) hL[t * SUB + threadIdx.x] = sL[threadIdx.x];
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+        const uint32_t a0 = sf[0][i], a1 = sf[1][i];
+        hrow[((size_t)t * SUB) * WIN + i] = (uint16_t)a0;
+        hrow[((size_t)t * SUB + 1) * WIN + i] = (uint16_t)a1;
+        if (i >= 1 && (a0 + a1)) atomicAdd(&wf[(int64_t)ni * WIN + i], a0 + a1);
+    }
+}
+
+// per half-tile count of elements going left: L_h + sum of the window bins
+// below the chosen boundary (warp per half-tile); nodes split by the slow path
+// (value not a window boundary) count from the data
+template <typename T>
+__global__ void k_tile_left(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap,
+                            DevCtx c, const Split* __restrict__ split, const uint16_t* __restrict__ hrow,
+                            const uint32_t* __restrict__ hL, uint32_t nhalf, uint32_t* __restrict__ tile_left) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t hb = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (hb >= nhalf) return;
+    const uint32_t t = hb / SUB, sub = hb % SUB;
+    const int ni = tmap[t];
+    const Split sp = split[ni];
+    uint32_t cnt = 0;
+    if (sp.status == ST_SPLIT) {
+        if (sp.wsel >= 0) {
+            for (int i = 1 + lane; i <= sp.wsel; i += 32) cnt += hrow[(size_t)hb * WIN + i];
+            cnt = warp_isum(cnt) + hL[hb];
+        } else {
+            const LNode nd = nodes[ni];
+            const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
+            const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
+            const T* row = src + (int64_t)sp.dim * c.N + nd.start;
+            for (int64_t e = e0 + lane; e < e1; e += 32) cnt += (double)row[e] < sp.value;
+            cnt = warp_isum(cnt);
         }
     }
-    __syncwarp();
-    if (lane < qn) search(q[warp][lane]);
-    for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
-    if (lane == 0 && lc) atomicAdd(&sL, (unsigned long long)lc);
-    __syncthreads();
-    if (threadIdx.x == 0 && sL) atomicAdd(&split[ni].L, sL);
-    for (int i = threadIdx.x + 1; i < nw; i += blockDim.x)
-        if (sf[i]) atomicAdd(&wf[(int64_t)ni * WIN + i], sf[i]);
+    if (lane == 0) tile_left[hb] = cnt;
 }
 
 // ============================================================================
@@ -638,6 +686,7 @@ __global__ void k_select(const LNode* __restrict__ nodes, int K, Split* split, c
             sp.status = ST_SPLIT;
             sp.value = (double)wb[(int64_t)ni * WIN + besti];
             sp.nl = bestc;
+            sp.wsel = besti;
         } else {
             sp.status = ST_SLOW;
             slow_list[atomicAdd(slow_count, 1)] = ni;
@@ -843,7 +892,7 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
         if (threadIdx.x == 0) {
             Split sp = split[ni];
             if (s_done) {
-                sp.status = ST_SPLIT; sp.dim = s_dim; sp.value = s_val; sp.nl = s_nl;
+                sp.status = ST_SPLIT; sp.dim = s_dim; sp.value = s_val; sp.nl = s_nl; sp.wsel = -1;
             } else {
                 sp.status = ST_LEAF;
             }
@@ -856,46 +905,6 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
 // ============================================================================
 // stable segmented partition (local_tree.py:183-233), coordinates + row ids
 // ============================================================================
-template <typename T>
-__global__ void __launch_bounds__(TILE_THREADS)
-k_count(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
-        const Split* __restrict__ split, uint32_t* tile_left) {
-    constexpr int EPT = TILE / TILE_THREADS;
-    __shared__ uint32_t red[SUB][TILE_THREADS / 32];
-    const uint32_t t = blockIdx.x;
-    const int ni = tmap[t];
-    const LNode nd = nodes[ni];
-    const Split sp = split[ni];
-    uint32_t cnt[SUB] = {};
-    if (sp.status == ST_SPLIT) {
-        const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
-        const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
-        const T* row = src + (int64_t)sp.dim * c.N + nd.start;
-        T v[EPT];
-#pragma unroll
-        for (int j = 0; j < EPT; j++) {
-            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-            v[j] = e < e1 ? row[e] : T(0);
-        }
-#pragma unroll
-        for (int j = 0; j < EPT; j++) {
-            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-            cnt[j / (EPT / SUB)] += (e < e1) && ((double)v[j] < sp.value);
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < SUB; u++) {
-        for (int o = 16; o > 0; o >>= 1) cnt[u] += __shfl_xor_sync(FULL, cnt[u], o);
-        if ((threadIdx.x & 31) == 0) red[u][threadIdx.x >> 5] = cnt[u];
-    }
-    __syncthreads();
-    if (threadIdx.x < SUB) {
-        uint32_t s = 0;
-        for (int w = 0; w < TILE_THREADS / 32; w++) s += red[threadIdx.x][w];
-        tile_left[t * SUB + threadIdx.x] = s;
-    }
-}
-
 // stable scatter of one tile: CH chunks of 256 elements per pass; every load of
 // a pass is issued before the single block-wide prefix over (chunk, warp) counts
 template <typename T, int DT, int CH>
@@ -1840,10 +1849,12 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         }
         int32_t* tmap = dalloc<int32_t>(tiles, st);
         k_tile_map<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tiles, tmap);
-        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, wb, wf);
+        uint16_t* hrow = dalloc<uint16_t>((size_t)tiles * SUB * WIN, st);
+        uint32_t* hL = dalloc<uint32_t>((size_t)tiles * SUB, st);
+        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, wb, wf, hrow, hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
-        k_count<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, tile_left);
+        k_tile_left<T><<<(tiles * SUB + 7) / 8, 256, 0, st>>>(lsrc, lv, tmap, c, split, hrow, hL, tiles * SUB, tile_left);
         size_t tmp_bytes = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
@@ -1873,7 +1884,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         tr.mark("level done", (int)levels.size());
         slow_total += *h_slow;
         ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
-        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st);
+        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st);
         dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
