@@ -271,12 +271,14 @@ def run_b200(args):
     clocks.start()
     evs = []
     levels = 0
+    slow_nodes = 0
     tree = None
     for _ in range(args.steps):
         del tree
         tree, out, ev = step()
         evs.append(ev)
         levels = tree.build_info["levels"]
+        slow_nodes = tree.build_info["slow_nodes"]
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -392,6 +394,7 @@ def run_b200(args):
                                  "counters": ctr_src}},
             "sample_check_vs_fp64_bruteforce": ok,
             "build_levels": levels,
+            "build_slow_nodes": slow_nodes,
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,

@@ -39,7 +39,7 @@
 namespace kdb {
 
 constexpr int MAXS = 1024;       // max sample size supported on device
-constexpr int WIN = 256;         // histogram window (boundaries)
+constexpr int WIN = 128;         // histogram window (boundaries around the sample median; +-4 sigma of its rank)
 constexpr int TILE = 4096;       // elements per tile CTA
 constexpr int TILE_THREADS = 256;
 constexpr int SUB = 2;  // partition half-tiles per tile (k_scatter moves one per CTA)
@@ -505,87 +505,155 @@ static __global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32
 // each half-tile's "left" count is L_h + sum(row_h[1..wsel]) (k_tile_left), so
 // the partition needs no second pass over the split column.
 // ============================================================================
+// one element global -> shared without a register round trip (cp.async, 4 or 8 bytes)
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// per tile of the level: node, element count and the offset of its split-dimension
+// values in the level's SoA buffer (k_hist streams tiles from these)
+struct TileInfo {
+    int32_t ni;
+    int32_t cnt;
+    int64_t off;
+};
+
+static __global__ void k_tile_info(const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap,
+                                   const Split* __restrict__ split, uint32_t tiles, int64_t N,
+                                   TileInfo* __restrict__ tinfo) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tiles) return;
+    const int ni = tmap[t];
+    const LNode nd = nodes[ni];
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
+    tinfo[t] = TileInfo{ni, (int32_t)max((int64_t)0, e1 - e0), (int64_t)split[ni].dim * N + nd.start + e0};
+}
+
+// Persistent: each CTA streams a contiguous run of tiles; the next tile's values
+// are copied into the other shared buffer (cp.async) while the current one is
+// classified, and the node's window / accumulators are only reloaded / flushed
+// when the run crosses into another node.
 template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS)
-k_hist(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c, Split* split,
+k_hist(const T* __restrict__ src, const TileInfo* __restrict__ tinfo, uint32_t tiles, Split* split,
        const T* __restrict__ wb, uint32_t* __restrict__ wf, uint16_t* __restrict__ hrow, uint32_t* __restrict__ hL) {
     constexpr int EPT = TILE / TILE_THREADS;
     constexpr int HPT = EPT / SUB;  // elements per thread in each half-tile
     constexpr int NW = TILE_THREADS / 32;
+    extern __shared__ __align__(16) unsigned char hist_dyn[];  // 2 tile buffers (dynamic: 64 KB for f64)
+    T (*buf)[TILE] = reinterpret_cast<T (*)[TILE]>(hist_dyn);
     __shared__ T sb[WIN];
     __shared__ uint32_t sf[SUB][WIN];
+    __shared__ uint32_t nacc[WIN];
     __shared__ T q[NW][64];  // per-warp queue of in-window values (keeps the searches warp-dense)
     __shared__ uint32_t sL[SUB];
-    const uint32_t t = blockIdx.x;
-    const int ni = tmap[t];
-    const LNode nd = nodes[ni];
-    const Split sp = split[ni];
-    const int nw = sp.whi - sp.wlo;
+    __shared__ unsigned long long nL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
-    const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
-    const T* row = src + (int64_t)sp.dim * c.N + nd.start;
-    // issue every load of the tile before touching shared memory
-    T v[EPT];
+    const uint32_t t0 = (uint32_t)((uint64_t)tiles * blockIdx.x / gridDim.x);
+    const uint32_t t1 = (uint32_t)((uint64_t)tiles * (blockIdx.x + 1) / gridDim.x);
+    if (t0 >= t1) return;
+    auto issue = [&](const TileInfo& ti, int slot) {
+        const T* g = src + ti.off;
 #pragma unroll
-    for (int j = 0; j < EPT; j++) {
-        const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-        v[j] = e < e1 ? row[e] : T(0);
-    }
-    // sb[i] = boundary i+1 for i < nw-2, +inf above: bin of x = 1 + #{i : sb[i] <= x}
-    for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
-        sf[0][i] = 0;
-        sf[1][i] = 0;
-        sb[i] = i < nw - 2 ? wb[(int64_t)ni * WIN + i + 1] : T(INFINITY);
-    }
-    if (threadIdx.x < SUB) sL[threadIdx.x] = 0;
-    const T lo_b = wb[(int64_t)ni * WIN], hi_b = wb[(int64_t)ni * WIN + nw - 1];
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < SUB; h++) {
-        uint32_t* hist = sf[h];
-        auto search = [&](T x) {  // branchless upper_bound of x in the boundaries 1 .. nw-2
-            int pos = 0;
-#pragma unroll
-            for (int step = WIN / 2; step > 0; step >>= 1)
-                if (sb[pos + step - 1] <= x) pos += step;
-            atomicAdd(&hist[1 + pos], 1u);
-        };
-        uint32_t lc = 0;
-        int qn = 0;  // warp-uniform queue length
-#pragma unroll
-        for (int jj = 0; jj < HPT; jj++) {
-            const int j = h * HPT + jj;
-            const int64_t e = e0 + j * TILE_THREADS + threadIdx.x;
-            const bool ok = e < e1;
-            const bool below = ok && v[j] < lo_b;
-            const bool inwin = ok && !below && v[j] < hi_b;
-            lc += below;
-            const unsigned m = __ballot_sync(FULL, inwin);
-            if (inwin) q[warp][qn + __popc(m & ((1u << lane) - 1))] = v[j];
-            qn += __popc(m);
-            if (qn >= 32) {  // one dense round of 32 searches
-                __syncwarp();
-                search(q[warp][qn - 32 + lane]);
-                qn -= 32;
-                __syncwarp();
-            }
+        for (int j = 0; j < EPT; j++) {
+            const int e = j * TILE_THREADS + threadIdx.x;
+            if (e < ti.cnt) cp_async_elem(&buf[slot][e], g + e);
         }
-        __syncwarp();
-        if (lane < qn) search(q[warp][lane]);
-        __syncwarp();
-        for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
-        if (lane == 0 && lc) atomicAdd(&sL[h], lc);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    TileInfo cur = tinfo[t0];
+    issue(cur, 0);
+    TileInfo nxt = t0 + 1 < t1 ? tinfo[t0 + 1] : TileInfo{-1, 0, 0};
+    int cur_ni = -1, nw = 0;
+    T lo_b = T(0), hi_b = T(0);
+    for (uint32_t t = t0, it = 0; t < t1; t++, it++) {
+        const int slot = it & 1;
+        if (t + 1 < t1) issue(nxt, slot ^ 1);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const TileInfo after = t + 2 < t1 ? tinfo[t + 2] : TileInfo{-1, 0, 0};
+        if (cur.ni != cur_ni) {
+            if (cur_ni >= 0) {  // flush the finished node
+                for (int i = threadIdx.x + 1; i < nw; i += blockDim.x)
+                    if (nacc[i]) atomicAdd(&wf[(int64_t)cur_ni * WIN + i], nacc[i]);
+                if (threadIdx.x == 0 && nL) atomicAdd(&split[cur_ni].L, nL);
+                __syncthreads();
+            }
+            cur_ni = cur.ni;
+            const Split sp = split[cur_ni];
+            nw = sp.whi - sp.wlo;
+            // sb[i] = boundary i+1 for i < nw-2, +inf above: bin of x = 1 + #{i : sb[i] <= x}
+            for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
+                nacc[i] = 0;
+                sb[i] = i < nw - 2 ? wb[(int64_t)cur_ni * WIN + i + 1] : T(INFINITY);
+            }
+            if (threadIdx.x == 0) nL = 0;
+            lo_b = wb[(int64_t)cur_ni * WIN];
+            hi_b = wb[(int64_t)cur_ni * WIN + nw - 1];
+        }
+        for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
+            sf[0][i] = 0;
+            sf[1][i] = 0;
+        }
+        if (threadIdx.x < SUB) sL[threadIdx.x] = 0;
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
+        const T* tb = buf[slot];
+#pragma unroll
+        for (int h = 0; h < SUB; h++) {
+            uint32_t* hist = sf[h];
+            auto search = [&](T x) {  // branchless upper_bound of x in the boundaries 1 .. nw-2
+                int pos = 0;
+#pragma unroll
+                for (int step = WIN / 2; step > 0; step >>= 1)
+                    if (sb[pos + step - 1] <= x) pos += step;
+                atomicAdd(&hist[1 + pos], 1u);
+            };
+            uint32_t lc = 0;
+            int qn = 0;  // warp-uniform queue length
+#pragma unroll
+            for (int jj = 0; jj < HPT; jj++) {
+                const int e = (h * HPT + jj) * TILE_THREADS + threadIdx.x;
+                const bool ok = e < cur.cnt;
+                const T v = tb[e];
+                const bool below = ok && v < lo_b;
+                const bool inwin = ok && !below && v < hi_b;
+                lc += below;
+                const unsigned m = __ballot_sync(FULL, inwin);
+                if (inwin) q[warp][qn + __popc(m & ((1u << lane) - 1))] = v;
+                qn += __popc(m);
+                if (qn >= 32) {  // one dense round of 32 searches
+                    __syncwarp();
+                    search(q[warp][qn - 32 + lane]);
+                    qn -= 32;
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            if (lane < qn) search(q[warp][lane]);
+            __syncwarp();
+            for (int o = 16; o > 0; o >>= 1) lc += __shfl_xor_sync(FULL, lc, o);
+            if (lane == 0 && lc) atomicAdd(&sL[h], lc);
+        }
+        __syncthreads();
+        if (threadIdx.x < SUB) hL[t * SUB + threadIdx.x] = sL[threadIdx.x];
+        if (threadIdx.x == 0) nL += sL[0] + sL[1];
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+            const uint32_t a0 = sf[0][i], a1 = sf[1][i];
+            hrow[((size_t)t * SUB) * WIN + i] = (uint16_t)a0;
+            hrow[((size_t)t * SUB + 1) * WIN + i] = (uint16_t)a1;
+            nacc[i] += a0 + a1;
+        }
+        __syncthreads();
+        cur = nxt;
+        nxt = after;
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && (sL[0] + sL[1])) atomicAdd(&split[ni].L, (unsigned long long)(sL[0] + sL[1]));
-    if (threadIdx.x < SUB) hL[t * SUB + threadIdx.x] = sL[threadIdx.x];
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
-        const uint32_t a0 = sf[0][i], a1 = sf[1][i];
-        hrow[((size_t)t * SUB) * WIN + i] = (uint16_t)a0;
-        hrow[((size_t)t * SUB + 1) * WIN + i] = (uint16_t)a1;
-        if (i >= 1 && (a0 + a1)) atomicAdd(&wf[(int64_t)ni * WIN + i], a0 + a1);
-    }
+    for (int i = threadIdx.x + 1; i < nw; i += blockDim.x)
+        if (nacc[i]) atomicAdd(&wf[(int64_t)cur_ni * WIN + i], nacc[i]);
+    if (threadIdx.x == 0 && nL) atomicAdd(&split[cur_ni].L, nL);
 }
 
 // per half-tile count of elements going left: L_h + sum of the window bins
@@ -911,22 +979,25 @@ template <typename T, int DT, int CH>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
           int32_t* __restrict__ idst, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
-          const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff) {
+          const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff, uint32_t nhalf) {
     constexpr int NW = TILE_THREADS / 32;
     constexpr int DC = DT > 0 ? DT : 16;
     __shared__ uint32_t wl[CH * NW];
     __shared__ uint32_t wpre[CH * NW];
-    const uint32_t t = blockIdx.x / SUB, sub = blockIdx.x % SUB;
+    const int D = DT > 0 ? DT : c.dims;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // persistent: a grid of resident CTAs strides over the half-tiles (empty second
+    // halves of small nodes cost a loop iteration, not a CTA launch)
+    for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x) {
+    const uint32_t t = hb / SUB, sub = hb % SUB;
     const int ni = tmap[t];
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
-    if (sp.status != ST_SPLIT) return;
-    const int D = DT > 0 ? DT : c.dims;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (sp.status != ST_SPLIT) continue;
     const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
     const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
-    if (e0 >= e1) return;
-    const uint32_t lbefore = tile_loff[blockIdx.x] - tile_loff[nd.tile_off * SUB];  // lefts earlier in this node
+    if (e0 >= e1) continue;
+    const uint32_t lbefore = tile_loff[hb] - tile_loff[nd.tile_off * SUB];  // lefts earlier in this node
     int64_t lrun = lbefore;
     int64_t rrun = e0 - lbefore;
     const int64_t N = c.N;
@@ -999,6 +1070,7 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
         lrun += ltot;
         rrun += pass_n - ltot;
         __syncthreads();
+    }
     }
 }
 
@@ -1399,13 +1471,6 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     out_nl = pickB ? cumB : cumA;
 }
 
-// one element global -> shared without a register round trip (cp.async, 4 or 8 bytes)
-template <typename T>
-__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
-    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
 
 template <typename T, int DT>
 __global__ void __launch_bounds__(32, 13)
@@ -1798,6 +1863,16 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         const char* e = std::getenv("KDB_SAMPLE_CTA_K");
         return e ? atoi(e) : 1024;
     }();
+    uint32_t scatter_grid = 0, hist_grid = 0;  // resident CTAs of the persistent scatter / histogram
+    {
+        int sms = 148, per = 0;
+        KD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, out->device));
+        KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scatter<T, 3, 8>, TILE_THREADS, 0));
+        scatter_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
+        KD_CUDA(cudaFuncSetAttribute(k_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * TILE * sizeof(T))));
+        KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hist<T>, TILE_THREADS, 2 * TILE * sizeof(T)));
+        hist_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
+    }
     int par = 0;  // buffer holding the current level's points
     int64_t slow_total = 0;
     int64_t max_node = n;  // largest node of the current level (read back with the level counters)
@@ -1851,7 +1926,10 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         k_tile_map<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tiles, tmap);
         uint16_t* hrow = dalloc<uint16_t>((size_t)tiles * SUB * WIN, st);
         uint32_t* hL = dalloc<uint32_t>((size_t)tiles * SUB, st);
-        k_hist<T><<<tiles, TILE_THREADS, 0, st>>>(lsrc, lv, tmap, c, split, wb, wf, hrow, hL);
+        TileInfo* tinfo = dalloc<TileInfo>(tiles, st);
+        k_tile_info<<<(tiles + 255) / 256, 256, 0, st>>>(lv, tmap, split, tiles, c.N, tinfo);
+        k_hist<T><<<std::min<uint32_t>(tiles, hist_grid), TILE_THREADS, 2 * TILE * sizeof(T), st>>>(lsrc, tinfo, tiles, split, wb, wf, hrow,
+                                                                                  hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
         k_tile_left<T><<<(tiles * SUB + 7) / 8, 256, 0, st>>>(lsrc, lv, tmap, c, split, hrow, hL, tiles * SUB, tile_left);
@@ -1860,8 +1938,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
-    k_scatter<T, DTV, CHV><<<tiles * SUB, TILE_THREADS, 0, st>>>(lsrc, lidx, buf[1 - par], idx[1 - par], lv, tmap, c, \
-                                                           split, tile_loff)
+    k_scatter<T, DTV, CHV><<<std::min<uint32_t>(tiles * SUB, scatter_grid), TILE_THREADS, 0, st>>>(                  \
+        lsrc, lidx, buf[1 - par], idx[1 - par], lv, tmap, c, split, tile_loff, tiles * SUB)
         switch (dims) {
             case 1: KD_SCATTER(1, 8); break;
             case 2: KD_SCATTER(2, 8); break;
@@ -1884,7 +1962,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         tr.mark("level done", (int)levels.size());
         slow_total += *h_slow;
         ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
-        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st);
+        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st);
         dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
