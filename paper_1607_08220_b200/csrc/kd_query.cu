@@ -596,6 +596,202 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     }
 }
 
+// ----------------------------------------------------------------------------
+// Warp per query for D >= 4.  In higher dimensions a query scans thousands of
+// buckets (C4: ~2.1K buckets, ~130K points per query) and neighbouring queries'
+// candidate sets differ, so one lane per query diverges and reads scattered
+// buckets, and a shared (packet) traversal blows up to the union of 32 queries'
+// candidates.  Here the whole warp serves one query: the traversal is executed
+// uniformly by every lane (no divergence), and a bucket is scanned with one
+// point per lane -- coalesced SoA loads, exact fp32 pre-filter per lane, the
+// survivors' binary64 distances (reference order) inserted by the warp in lane
+// order into a top-k list that every lane holds.  Queries are taken in home-
+// leaf order from a global counter (persistent warps).
+// ----------------------------------------------------------------------------
+constexpr int WQ_WARPS = 4;
+constexpr int WQ_DC = 16;  // max dimensions
+
+template <typename T, int KM>
+__global__ void __launch_bounds__(WQ_WARPS * 32)
+k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
+         const uint64_t* __restrict__ ids, int64_t n, int D, const double* __restrict__ queries,
+         const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
+         const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
+         int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
+    constexpr int DC = WQ_DC;
+    __shared__ int s_node[WQ_WARPS][QCAP];
+    __shared__ float s_off[WQ_WARPS][QCAP][32];
+    __shared__ double s_q[WQ_WARPS][DC];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool has_ex = excl != nullptr;
+    const int kk = k + (has_ex ? 1 : 0);  // top-(k+1) minus the excluded id (see k_knn_persist)
+    // box offsets are lane-distributed: lane d holds the offset along dimension d
+    // (lanes >= D hold 0); a bound is a round-toward-zero warp sum of squares --
+    // rounded down in any order, so still <= every point's binary64 distance
+    auto bound_of = [&](float o) {
+        float b = __fmul_rz(o, o);
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) b = __fadd_rz(b, __shfl_xor_sync(FULL, b, s));
+        // lanes may associate the butterfly differently: lane 0's value for everyone
+        // keeps the traversal warp-uniform
+        return __shfl_sync(FULL, b, 0);
+    };
+    for (;;) {
+        long long slot = 0;
+        if (lane == 0) slot = (long long)atomicAdd(counter, 1ULL);
+        slot = __shfl_sync(FULL, slot, 0);
+        if (slot >= nq) break;
+        const int64_t qi = order ? (int64_t)order[slot] : slot;
+        const double* qrow = queries + qi * D;
+        const double radius = radii ? radii[qi] : INFINITY;
+        const uint64_t ex = has_ex ? excl[qi] : ~0ULL;
+        const double qmine = lane < D ? qrow[lane] : 0.0;  // lane d: q[d]
+        if (lane < DC) s_q[warp][lane] = qmine;
+        double qq = qmine * qmine;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) qq += __shfl_xor_sync(FULL, qq, s);
+        __syncwarp();
+        float q32[DC];
+#pragma unroll
+        for (int d = 0; d < DC; d++) q32[d] = __double2float_rn(s_q[warp][d]);
+        const double qnorm = sqrt(qq) * (1.0 + 1e-12);
+        auto make_thr = [&](double R) {  // exact fp32 pre-filter threshold (derivation at k_knn_persist)
+            if (!(R < 1e300)) return INFINITY;
+            const double u = 5.9604644775390625e-08;
+            const double x = R * (1.0 + 1e-15);
+            const double uq = u * qnorm;
+            const double t = (x + 2.0 * uq * uq + 2.0 * uq * sqrt(x + uq * uq)) * (1.0 + (D + 2) * u) /
+                             ((1.0 - 2.0 * u) * (1.0 - 2.0 * u)) * (1.0 + 1e-12);
+            return t >= 3.0e38 ? INFINITY : __double2float_ru(t);
+        };
+        double bd[KM];
+        uint32_t bp[KM];
+        int cnt = 0;
+        double kth_d = radius;
+        uint32_t kth_p = 0;
+        float thr32 = sizeof(T) == 4 ? make_thr(radius) : INFINITY;
+        int64_t c0 = 0, c1 = 0, c2 = 0;
+        float off = 0.0f;  // this lane's dimension
+        auto admissible = [&](float b) {
+            const double bb = (double)b;
+            return cnt < kk ? bb < radius : bb <= kth_d;
+        };
+        int node = n_nodes > 0 ? 0 : -1;
+        int sp = 0;
+        while (node >= 0) {
+            c0++;
+            const KdNode rec = nodes[node];
+            if (rec.db >= 0) {
+                const int dim = rec.db;
+                const double qd = s_q[warp][dim];
+                const bool goleft = qd < rec.v;
+                const int near = goleft ? node + 1 : rec.a;
+                const int far = goleft ? rec.a : node + 1;
+                const float ad = __double2float_rz(fabs(qd - rec.v));
+                const float of = lane == dim ? ad : off;
+                if (admissible(bound_of(lane < D ? of : 0.0f)) && sp < QCAP) {
+                    s_off[warp][sp][lane] = of;
+                    if (lane == 0) s_node[warp][sp] = far;
+                    sp++;
+                }
+                node = near;
+                continue;
+            }
+            // bucket: one point per lane per round
+            const int start = rec.a, len = -1 - rec.db;
+            c1++;
+            c2 += len;
+            for (int c = 0; c < len; c += 32) {
+                const int j = c + lane;
+                const bool valid = j < len;
+                T cv[DC];
+#pragma unroll
+                for (int d = 0; d < DC; d++)
+                    if (d < D) cv[d] = valid ? coords[(int64_t)d * n + start + j] : T(0);
+                bool pass = valid;
+                if constexpr (sizeof(T) == 4) {
+                    float d32 = 0.0f;
+#pragma unroll
+                    for (int d = 0; d < DC; d++) {
+                        if (d < D) {
+                            const float tt = cv[d] - q32[d];
+                            d32 = fmaf(tt, tt, d32);
+                        }
+                    }
+                    pass = pass && !(d32 > thr32);
+                }
+                double dist = INFINITY;
+                if (pass) {
+                    dist = 0.0;
+#pragma unroll
+                    for (int d = 0; d < DC; d++) {
+                        if (d < D) {
+                            const double df = __dsub_rn((double)cv[d], s_q[warp][d]);
+                            dist = __dadd_rn(dist, __dmul_rn(df, df));
+                        }
+                    }
+                    pass = cnt < kk ? dist < radius : dist <= kth_d;
+                }
+                unsigned m = __ballot_sync(FULL, pass);
+                while (m) {  // survivors in point order, inserted uniformly by every lane
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const double dd = __shfl_sync(FULL, dist, src);
+                    const uint32_t pos = (uint32_t)(start + c + src);
+                    if (cnt < kk ? dd < radius : (dd <= kth_d && lexless_pos(dd, pos, kth_d, kth_p, ids))) {
+                        topk_insert_pos<KM>(bd, bp, cnt, kk, dd, pos, ids);
+                        if (cnt == kk) {
+#pragma unroll
+                            for (int jj = 0; jj < KM; jj++)
+                                if (jj == kk - 1) { kth_d = bd[jj]; kth_p = bp[jj]; }
+                            if constexpr (sizeof(T) == 4) thr32 = make_thr(kth_d);
+                        }
+                    }
+                }
+            }
+            // next admissible far child
+            node = -1;
+            while (sp > 0) {
+                sp--;
+                const float po = s_off[warp][sp][lane];
+                if (admissible(bound_of(lane < D ? po : 0.0f))) {
+                    node = s_node[warp][sp];
+                    off = po;
+                    break;
+                }
+                c0++;
+            }
+        }
+        // results (lane w writes row entry w)
+        int w = 0;
+        bool dropped = false;
+#pragma unroll
+        for (int j = 0; j < KM; j++) {
+            if (j < cnt) {
+                const uint64_t id = ids[bp[j]];
+                if (has_ex && !dropped && id == ex) {
+                    dropped = true;
+                } else if (w < k) {
+                    if (lane == w) {
+                        out_d[qi * (int64_t)k + w] = bd[j];
+                        out_i[qi * (int64_t)k + w] = id;
+                    }
+                    w++;
+                }
+            }
+        }
+        if (lane == 0) {
+            out_c[qi] = w;
+            if (out_ctr) {
+                out_ctr[qi * 3 + 0] = c0;
+                out_ctr[qi * 3 + 1] = c1;
+                out_ctr[qi * 3 + 2] = c2;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // leaf reached by descending with the tie rule (coord >= value goes right);
 // used as the sort key that makes each warp's 32 queries spatially coherent
 template <int DT>
@@ -654,6 +850,24 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
                        cudaStream_t st) {
     const int threads = 128;
     const unsigned blocks = (unsigned)((a.nq + threads - 1) / threads);
+    if constexpr (KM > 0 && DT == 0) {
+        if (!a.thread_per_query && t.dims <= WQ_DC) {
+            int dev = 0, sms = 148, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_wq<T, KM>, WQ_WARPS * 32, 0);
+            const long long want = (a.nq + WQ_WARPS - 1) / WQ_WARPS;
+            const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
+            unsigned long long* ctr = nullptr;
+            KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
+            KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+            k_knn_wq<T, KM><<<grid, WQ_WARPS * 32, 0, st>>>(
+                t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
+                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
+            cudaFreeAsync(ctr, st);
+            return;
+        }
+    }
     if constexpr (KM > 0) {
         if (!a.thread_per_query) {
             int dev = 0, sms = 148, per_sm = 0;
