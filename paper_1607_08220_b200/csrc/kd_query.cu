@@ -70,6 +70,9 @@ __device__ __forceinline__ bool lexless_pos(double d0, uint32_t p0, double d1, u
     return d0 < d1 || (d0 == d1 && ids[p0] < ids[p1]);
 }
 
+// insert into the ascending (d, packed row) list of capacity k <= KM (the caller
+// has checked that it enters): one descending pass, each slot keeps, shifts from
+// its predecessor, or takes the new entry; ids are read only on exact ties
 template <int KM>
 __device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
                                                 uint32_t p, const uint64_t* __restrict__ ids) {
@@ -79,7 +82,7 @@ __device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)
     for (int jj = KM - 1; jj >= 0; jj--) {
         if (jj <= last && !placed) {
             const int pj = jj > 0 ? jj - 1 : 0;
-            const bool shift = jj > 0 && lexless_pos(d, p, bd[pj], bp[pj], ids);
+            const bool shift = jj > 0 && (d < bd[pj] || (d == bd[pj] && ids[p] < ids[bp[pj]]));
             if (shift) {
                 bd[jj] = bd[pj];
                 bp[jj] = bp[pj];
@@ -91,6 +94,20 @@ __device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)
         }
     }
     if (cnt < k) cnt++;
+}
+
+// slot k-1 of the list (a register move when the list is exactly k long)
+template <int KM>
+__device__ __forceinline__ void topk_last(const double (&bd)[KM], const uint32_t (&bp)[KM], int k, double& kd,
+                                          uint32_t& kp) {
+    if (k == KM) {
+        kd = bd[KM - 1];
+        kp = bp[KM - 1];
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < KM; j++)
+        if (j == k - 1) { kd = bd[j]; kp = bp[j]; }
 }
 
 template <int DT>
@@ -423,6 +440,8 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 cnt = 0;
                 kth_d = radius;
                 kth_p = 0;
+#pragma unroll
+                for (int j = 0; j < KM; j++) bd[j] = INFINITY;
                 c0 = c1 = c2 = 0;
                 if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
                     double qq = 0.0;
@@ -494,18 +513,11 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
             const int start = lstart, len = llen;
             c1++;
             c2 += len;
-            // software-pipelined: the next point's coordinates are in flight
-            // while this one is evaluated
-            T cv[DC], nv[DC];
-#pragma unroll
-            for (int d = 0; d < DC; d++)
-                if (d < D) cv[d] = coords[(int64_t)d * n + start];
             for (int i = start; i < start + len; i++) {
-                if (i + 1 < start + len) {
+                T cv[DC];
 #pragma unroll
-                    for (int d = 0; d < DC; d++)
-                        if (d < D) nv[d] = coords[(int64_t)d * n + i + 1];
-                }
+                for (int d = 0; d < DC; d++)
+                    if (d < D) cv[d] = coords[(int64_t)d * n + i];
                 bool take = true;
                 if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) {
                     float d32 = 0.0f;
@@ -531,15 +543,11 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                                  : (dist <= kth_d && lexless_pos(dist, (uint32_t)i, kth_d, kth_p, ids))) {
                         topk_insert_pos<KM>(bd, bp, cnt, kk, dist, (uint32_t)i, ids);
                         if (cnt == kk) {
-#pragma unroll
-                            for (int j = 0; j < KM; j++)
-                                if (j == kk - 1) { kth_d = bd[j]; kth_p = bp[j]; }
+                            topk_last<KM>(bd, bp, kk, kth_d, kth_p);
                             if constexpr (kPersistF32Filter<DT> && sizeof(T) == 4) thr32 = make_thr(kth_d);
                         }
                     }
                 }
-#pragma unroll
-                for (int d = 0; d < DC; d++) cv[d] = nv[d];
             }
         }
         // ---- after the home leaf: restart from the root with a real k-th distance
@@ -666,6 +674,8 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
         };
         double bd[KM];
         uint32_t bp[KM];
+#pragma unroll
+        for (int j = 0; j < KM; j++) { bd[j] = INFINITY; bp[j] = 0; }
         int cnt = 0;
         double kth_d = radius;
         uint32_t kth_p = 0;
@@ -741,9 +751,7 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                     if (cnt < kk ? dd < radius : (dd <= kth_d && lexless_pos(dd, pos, kth_d, kth_p, ids))) {
                         topk_insert_pos<KM>(bd, bp, cnt, kk, dd, pos, ids);
                         if (cnt == kk) {
-#pragma unroll
-                            for (int jj = 0; jj < KM; jj++)
-                                if (jj == kk - 1) { kth_d = bd[jj]; kth_p = bp[jj]; }
+                            topk_last<KM>(bd, bp, kk, kth_d, kth_p);
                             if constexpr (sizeof(T) == 4) thr32 = make_thr(kth_d);
                         }
                     }
