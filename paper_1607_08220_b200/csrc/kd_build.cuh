@@ -1287,6 +1287,17 @@ __device__ __noinline__ int sub_exact_dim(const T* cs, const uint16_t* pm, int n
     return best;
 }
 
+// half_diff(b, n) < half_diff(a, n) exactly as the reference evaluates it
+// (median.py:160): distinct |2c - n| differ by >= 1/(2n) in the exact values,
+// far above the binary64 rounding of c/n, so the integers decide; only exact
+// mirror ties (a + b == n) need the rounded divisions
+__device__ __forceinline__ bool closer_to_half(int64_t b, int64_t a, int64_t n) {
+    const int64_t db = 2 * b - n, da = 2 * a - n;
+    const int64_t ab = db < 0 ? -db : db, aa = da < 0 ? -da : da;
+    if (ab != aa) return ab < aa;
+    return half_diff(b, n) < half_diff(a, n);
+}
+
 // Small nodes (n <= 32*SR, fixed dimension count): the node's points are read
 // once into registers; per-dimension sums come from registers and the split
 // dimension's keys are sorted by the unrolled network (warp_sort_t) instead of
@@ -1307,6 +1318,41 @@ __device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm,
 #pragma unroll
         for (int d = 0; d < DT; d++) x[d][r] = cs[d * ts + q];
     }
+    // per dimension: min/max key (constant?), shifted binary64 sums; the four
+    // reductions of every dimension run interleaved (one butterfly)
+    Key kmn[DT], kmx[DT];
+    double s1[DT], sq[DT];
+#pragma unroll
+    for (int d = 0; d < DT; d++) {
+        const double x0 = (double)__shfl_sync(FULL, x[d][0], 0);
+        kmn[d] = ~(Key)0;
+        kmx[d] = 0;
+        s1[d] = 0.0;
+        sq[d] = 0.0;
+#pragma unroll
+        for (int r = 0; r < SR; r++) {
+            if (r * 32 + lane < n) {
+                const Key k = tkey(x[d][r]);
+                kmn[d] = k < kmn[d] ? k : kmn[d];
+                kmx[d] = k > kmx[d] ? k : kmx[d];
+                const double y = __dsub_rn((double)x[d][r], x0);
+                s1[d] = __dadd_rn(s1[d], y);
+                sq[d] = __dadd_rn(sq[d], __dmul_rn(y, y));
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int d = 0; d < DT; d++) {
+            const Key a = __shfl_xor_sync(FULL, kmn[d], o), b = __shfl_xor_sync(FULL, kmx[d], o);
+            kmn[d] = a < kmn[d] ? a : kmn[d];
+            kmx[d] = b > kmx[d] ? b : kmx[d];
+            s1[d] = __dadd_rn(s1[d], __shfl_xor_sync(FULL, s1[d], o));
+            sq[d] = __dadd_rn(sq[d], __shfl_xor_sync(FULL, sq[d], o));
+        }
+    }
+    const double rn = 1.0 / (double)n;
     int best = -1;
     double bs = 0.0, be = 0.0;
     double s2v[DT], eb[DT];
@@ -1315,33 +1361,12 @@ __device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm,
     for (int d = 0; d < DT; d++) {
         s2v[d] = 0.0;
         eb[d] = 0.0;
-        const double x0 = (double)__shfl_sync(FULL, x[d][0], 0);
-        Key kmn = ~(Key)0, kmx = 0;
-        double s1 = 0.0, sq = 0.0;
-#pragma unroll
-        for (int r = 0; r < SR; r++) {
-            if (r * 32 + lane < n) {
-                const Key k = tkey(x[d][r]);
-                kmn = k < kmn ? k : kmn;
-                kmx = k > kmx ? k : kmx;
-                const double y = __dsub_rn((double)x[d][r], x0);
-                s1 = __dadd_rn(s1, y);
-                sq = __dadd_rn(sq, __dmul_rn(y, y));
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const Key a = __shfl_xor_sync(FULL, kmn, o), b = __shfl_xor_sync(FULL, kmx, o);
-            kmn = a < kmn ? a : kmn;
-            kmx = b > kmx ? b : kmx;
-        }
-        if (kmn == kmx) continue;
+        if (kmn[d] == kmx[d]) continue;
         ncmask |= 1u << d;
-        s1 = warp_sum(s1);
-        sq = warp_sum(sq);
-        const double bb = __dmul_rn(s1, s1) / (double)n;
-        s2v[d] = sq - bb;
-        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq + bb) + 1e-300;
+        const double bb = __dmul_rn(__dmul_rn(s1[d], s1[d]), rn);
+        s2v[d] = sq[d] - bb;
+        // + 4u*bb: the reciprocal product instead of a correctly rounded division
+        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq[d] + bb) + 4.0 * U64 * bb + 1e-300;
         if (best < 0 || s2v[d] > bs) { best = d; bs = s2v[d]; be = eb[d]; }
     }
     out_dim = -1;
@@ -1385,7 +1410,7 @@ __device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm,
     bool pickB;
     if (cumA == 0) pickB = true;
     else if (cumB >= n) pickB = false;
-    else pickB = half_diff(cumB, n) < half_diff(cumA, n);
+    else pickB = closer_to_half(cumB, cumA, n);
     out_dim = best;
     out_val = pickB ? (double)key_inv(nx, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
     out_nl = pickB ? cumB : cumA;
@@ -1402,49 +1427,69 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     constexpr int DC = DT > 0 ? DT : 16;
     const int D = DT > 0 ? DT : dims_rt;
     const int lane = threadIdx.x & 31;
-    // per dimension: constant?, binary64 sum of squared deviations + bound
+    // per dimension: constant?, binary64 sum of squared deviations + bound.  One
+    // pass over the node reads each point's index once for every dimension
+    // (shifted sums y = x - x0, x0 = the node's first point; S2 = sum y^2 - (sum y)^2 / n),
+    // then the reductions of all dimensions run interleaved.
+    Key kmins[DC], kmaxs[DC];
+    double s1[DC], sq[DC], x0[DC];
+    {
+        const int q0 = pm[0];
+#pragma unroll
+        for (int d = 0; d < DC; d++) {
+            x0[d] = d < D ? (double)cs[d * ts + q0] : 0.0;
+            kmins[d] = ~(Key)0;
+            kmaxs[d] = 0;
+            s1[d] = 0.0;
+            sq[d] = 0.0;
+        }
+    }
+#pragma unroll 2
+    for (int i = lane; i < n; i += 32) {
+        const int qv = pm[i];
+#pragma unroll
+        for (int d = 0; d < DC; d++) {
+            if (d < D) {
+                const T v = cs[d * ts + qv];
+                const Key k = tkey(v);
+                kmins[d] = k < kmins[d] ? k : kmins[d];
+                kmaxs[d] = k > kmaxs[d] ? k : kmaxs[d];
+                const double y = __dsub_rn((double)v, x0[d]);
+                s1[d] = __dadd_rn(s1[d], y);
+                sq[d] = __dadd_rn(sq[d], __dmul_rn(y, y));
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int d = 0; d < DC; d++) {
+            if (d < D) {
+                const Key a = __shfl_xor_sync(FULL, kmins[d], o), b = __shfl_xor_sync(FULL, kmaxs[d], o);
+                kmins[d] = a < kmins[d] ? a : kmins[d];
+                kmaxs[d] = b > kmaxs[d] ? b : kmaxs[d];
+                s1[d] = __dadd_rn(s1[d], __shfl_xor_sync(FULL, s1[d], o));
+                sq[d] = __dadd_rn(sq[d], __shfl_xor_sync(FULL, sq[d], o));
+            }
+        }
+    }
+    const double rn = 1.0 / (double)n;
     int best = -1;
     double bs = 0.0, be = 0.0;
     double s2v[DC], eb[DC];
-    Key kmins[DC], kmaxs[DC];
     unsigned ncmask = 0;
 #pragma unroll
     for (int d = 0; d < DC; d++) {
         s2v[d] = 0.0;
         eb[d] = 0.0;
-        if (d >= D) continue;
-        const T* row = cs + d * ts;
-        // one pass: shifted sums y = x - x0 (x0 = node's first value); S2 = sum y^2 - (sum y)^2 / n
-        const double x0 = (double)row[pm[0]];
-        Key kmn = ~(Key)0, kmx = 0;
-        double s1 = 0.0, sq = 0.0;
-#pragma unroll 4
-        for (int i = lane; i < n; i += 32) {
-            const T v = row[pm[i]];
-            const Key k = tkey(v);
-            kmn = k < kmn ? k : kmn;
-            kmx = k > kmx ? k : kmx;
-            const double y = __dsub_rn((double)v, x0);
-            s1 = __dadd_rn(s1, y);
-            sq = __dadd_rn(sq, __dmul_rn(y, y));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const Key a = __shfl_xor_sync(FULL, kmn, o), b = __shfl_xor_sync(FULL, kmx, o);
-            kmn = a < kmn ? a : kmn;
-            kmx = b > kmx ? b : kmx;
-        }
-        kmins[d] = kmn;
-        kmaxs[d] = kmx;
-        if (kmn == kmx) continue;
+        if (d >= D || kmins[d] == kmaxs[d]) continue;
         ncmask |= 1u << d;
-        s1 = warp_sum(s1);
-        sq = warp_sum(sq);
-        const double bb = __dmul_rn(s1, s1) / (double)n;
-        s2v[d] = sq - bb;
+        const double bb = __dmul_rn(__dmul_rn(s1[d], s1[d]), rn);
+        s2v[d] = sq[d] - bb;
         // rigorous bound on |computed - reference two-pass value| (both vs the exact sum of
         // squared deviations): shifted-sum rounding + the reference's own two-pass error
-        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq + bb) + 1e-300;
+        // (+ 4u*bb for the reciprocal product)
+        eb[d] = 4.0 * ((double)n + 8.0) * U64 * (sq[d] + bb) + 4.0 * U64 * bb + 1e-300;
         if (best < 0 || s2v[d] > bs) { best = d; bs = s2v[d]; be = eb[d]; }
     }
     out_dim = -1;
@@ -1465,7 +1510,7 @@ __device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int di
     bool pickB;
     if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
     else if (cumB >= n) pickB = false;    // no boundary after A
-    else pickB = half_diff(cumB, n) < half_diff(cumA, n);
+    else pickB = closer_to_half(cumB, cumA, n);
     out_dim = best;
     out_val = pickB ? (double)key_inv(nxt, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
     out_nl = pickB ? cumB : cumA;
