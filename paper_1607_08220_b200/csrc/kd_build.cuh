@@ -978,7 +978,7 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
 template <typename T, int DT, int CH>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
-          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap, DevCtx c,
+          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, const TileInfo* __restrict__ tinfo, DevCtx c,
           const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff, uint32_t nhalf) {
     constexpr int NW = TILE_THREADS / 32;
     constexpr int DC = DT > 0 ? DT : 16;
@@ -990,7 +990,9 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
     // halves of small nodes cost a loop iteration, not a CTA launch)
     for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x) {
     const uint32_t t = hb / SUB, sub = hb % SUB;
-    const int ni = tmap[t];
+    const TileInfo ti = tinfo[t];
+    if ((int)sub * (TILE / SUB) >= ti.cnt) continue;  // empty second half of a small node: one load
+    const int ni = ti.ni;
     const LNode nd = nodes[ni];
     const Split sp = split[ni];
     if (sp.status != ST_SPLIT) continue;
@@ -1984,7 +1986,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
     k_scatter<T, DTV, CHV><<<std::min<uint32_t>(tiles * SUB, scatter_grid), TILE_THREADS, 0, st>>>(                  \
-        lsrc, lidx, buf[1 - par], idx[1 - par], lv, tmap, c, split, tile_loff, tiles * SUB)
+        lsrc, lidx, buf[1 - par], idx[1 - par], lv, tinfo, c, split, tile_loff, tiles * SUB)
         switch (dims) {
             case 1: KD_SCATTER(1, 8); break;
             case 2: KD_SCATTER(2, 8); break;
