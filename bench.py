@@ -454,14 +454,19 @@ def run_b200_multi(args):
         e[2].record(stream)
         return tree, out, e, st, stats
 
+    tree = out = None
     for _ in range(args.warmup):
-        step()
+        del tree, out
+        tree, out, _, _, _ = step()
     torch.cuda.synchronize(); dist.barrier(); torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
     evs, moved, fwd = [], 0, 0
+    levels = 0
     for _ in range(args.steps):
+        del tree, out  # free the previous step's tree and results before building the next
         tree, out, e, st, stats = step()
+        levels = tree.build_info["levels"]
         evs.append(e)
         moved += st["points_moved"]
         fwd += stats.get("queries_forwarded", 0)
@@ -513,7 +518,9 @@ def run_b200_multi(args):
                          "model": f"N*L*(8D+12) per GPU, L={levels_model}"},
             "knn": {"value": world * q / tq, "unit": "queries/s"},
             "points_moved_per_step": int(tot[0].item()), "queries_forwarded_per_step": int(tot[1].item()),
-            "gpu_launches": None, "clocks": clk,
+            # local build (12 per level + 11) + global tier (4 per global level) + query
+            # (home-leaf keys, radix sort, KNN; route x2; remote KNN)
+            "gpu_launches": 12 * levels + 11 + 4 * (world.bit_length() - 1) + 12, "clocks": clk,
             "e2e": {"value": world * n / te_m / 1e6, "unit": "Mpoints/s (build + query, host in/out)",
                     "h2d_bytes_per_step": int(n * w.dims * 4 + q * w.dims * 8),
                     "d2h_bytes_per_step": int(q * w.k * 16), "ms_step": te_m * 1e3},

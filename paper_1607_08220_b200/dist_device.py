@@ -100,6 +100,12 @@ def rank_query_device(comm, tree, regions: DeviceRegions, qids, q, k: int, excl=
     p = comm.size
     me = comm.rank
     nq = q.shape[0]
+    if p == 1:  # one rank owns every query: the local search is the answer
+        if nq and tree.count:
+            d, i, c, _ = find_knn_device(tree, q.contiguous(), k, exclude_ids=excl)
+            return d, i, c
+        return (torch.zeros((nq, k), dtype=torch.float64, device=dev), torch.zeros((nq, k), dtype=torch.int64, device=dev),
+                torch.zeros(nq, dtype=torch.int64, device=dev))
     local_pos = torch.arange(nq, device=dev, dtype=torch.int64)
     ex = excl if excl is not None else torch.full((nq,), -1, dtype=torch.int64, device=dev)
     # 1. route to owners
@@ -120,18 +126,18 @@ def rank_query_device(comm, tree, regions: DeviceRegions, qids, q, k: int, excl=
         ld = torch.zeros((m, k), dtype=torch.float64, device=dev)
         li = torch.zeros((m, k), dtype=torch.int64, device=dev)
         lc = torch.zeros(m, dtype=torch.int64, device=dev)
-    rp = torch.where(lc == k, ld[:, k - 1], torch.full_like(ld[:, 0], float("inf"))) if m else ld[:, 0]
-    cand_q = [torch.arange(m, device=dev).repeat_interleave(k)]
-    slot_ok = (torch.arange(k, device=dev)[None, :] < lc[:, None]).reshape(-1)
-    cand_d, cand_i = [ld.reshape(-1)], [li.reshape(-1)]
+    md, mi, mc = ld, li, lc  # queries nobody else can improve keep their local rows
     forwarded = 0
     n_req = 0
     if p > 1:
+        rp = torch.where(lc == k, ld[:, k - 1], torch.full_like(ld[:, 0], float("inf"))) if m else ld[:, 0]
         # 3. forward to ranks within r'
         _, within = regions.route(o_q, radii=rp.contiguous(), want_within=True)
-        forwarded = int((within != 0).sum())
-        bits = ((within[:, None] >> torch.arange(p, device=dev)[None, :]) & 1).bool()  # (m, p)
-        rq, rr = torch.nonzero(bits, as_tuple=True)
+        fq = torch.nonzero(within != 0).flatten()  # owned queries with requests (ascending)
+        forwarded = int(fq.shape[0])
+        bits = ((within[fq][:, None] >> torch.arange(p, device=dev)[None, :]) & 1).bool()  # (f, p)
+        rf, rr = torch.nonzero(bits, as_tuple=True)
+        rq = fq[rf]
         n_req = int(rq.shape[0])
         req = _split_by(rr, p, rq, o_q[rq], rp[rq], o_ex[rq])
         inbox = comm.alltoall(req)
@@ -148,27 +154,42 @@ def rank_query_device(comm, tree, regions: DeviceRegions, qids, q, k: int, excl=
                 cc = torch.zeros(tq.shape[0], dtype=torch.int64, device=dev)
             replies[s] = (tq, dd, ii, cc)
         back = comm.alltoall(replies)
-        for s in sorted(back):
-            tq, dd, ii, cc = back[s]
-            cand_q.append(tq.repeat_interleave(k))
-            cand_d.append(dd.reshape(-1))
-            cand_i.append(ii.reshape(-1))
-            slot_ok = torch.cat([slot_ok, (torch.arange(k, device=dev)[None, :] < cc[:, None]).reshape(-1)])
-    # 5. merge (sq_dist, id), keep k, return rows to the ingesting rank
-    cq, cd, ci = torch.cat(cand_q), torch.cat(cand_d), torch.cat(cand_i)
-    cq, cd, ci = cq[slot_ok], cd[slot_ok], ci[slot_ok]
-    # uint64 order == int64 order of the bits for ids < 2^63
-    md, mi, mc = _merge_topk(cq, cd, ci, m, k)
-    home = _split_by(src_of, p, o_pos, md, mi, mc)
-    ret = comm.alltoall(home) if p > 1 else home
-    out_d = torch.zeros((nq, k), dtype=torch.float64, device=dev)
-    out_i = torch.zeros((nq, k), dtype=torch.int64, device=dev)
-    out_c = torch.zeros(nq, dtype=torch.int64, device=dev)
-    for s in ret:
-        pos, dd, ii, cc = ret[s]
-        out_d[pos] = dd
-        out_i[pos] = ii
-        out_c[pos] = cc
+        # 5. merge (sq_dist, id) for the forwarded queries only (local slot f = position in fq)
+        if forwarded:
+            slot_of = torch.full((m,), -1, dtype=torch.int64, device=dev)
+            slot_of[fq] = torch.arange(forwarded, device=dev)
+            karange = torch.arange(k, device=dev)
+            cand_q = [torch.arange(forwarded, device=dev).repeat_interleave(k)]
+            cand_d, cand_i = [ld[fq].reshape(-1)], [li[fq].reshape(-1)]
+            ok = [(karange[None, :] < lc[fq][:, None]).reshape(-1)]
+            for s in sorted(back):
+                tq, dd, ii, cc = back[s]
+                cand_q.append(slot_of[tq].repeat_interleave(k))
+                cand_d.append(dd.reshape(-1))
+                cand_i.append(ii.reshape(-1))
+                ok.append((karange[None, :] < cc[:, None]).reshape(-1))
+            okm = torch.cat(ok)
+            cq, cd, ci = torch.cat(cand_q)[okm], torch.cat(cand_d)[okm], torch.cat(cand_i)[okm]
+            # uint64 order == int64 order of the bits for ids < 2^63
+            fd, fi, fc = _merge_topk(cq, cd, ci, forwarded, k)
+            md, mi, mc = ld.clone(), li.clone(), lc.clone()
+            md[fq], mi[fq], mc[fq] = fd, fi, fc
+    if p == 1:
+        out_d, out_i, out_c = torch.zeros((nq, k), dtype=torch.float64, device=dev), \
+            torch.zeros((nq, k), dtype=torch.int64, device=dev), torch.zeros(nq, dtype=torch.int64, device=dev)
+        out_d[o_pos], out_i[o_pos], out_c[o_pos] = md, mi, mc
+    else:
+        # return rows to the ingesting rank
+        home = _split_by(src_of, p, o_pos, md, mi, mc)
+        ret = comm.alltoall(home)
+        out_d = torch.zeros((nq, k), dtype=torch.float64, device=dev)
+        out_i = torch.zeros((nq, k), dtype=torch.int64, device=dev)
+        out_c = torch.zeros(nq, dtype=torch.int64, device=dev)
+        for s in ret:
+            pos, dd, ii, cc = ret[s]
+            out_d[pos] = dd
+            out_i[pos] = ii
+            out_c[pos] = cc
     if stats is not None:
         stats["queries_forwarded"] = stats.get("queries_forwarded", 0) + forwarded
         stats["requests_sent"] = stats.get("requests_sent", 0) + n_req

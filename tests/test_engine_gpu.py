@@ -68,7 +68,7 @@ def test_unsplittable_raises():
         build_global_tree(parts, ClusterConfig(seed=0))
 
 
-@pytest.mark.parametrize("p", [1, 2, 4])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
 def test_device_resident_protocol(p, oracle):
     """dist_device.rank_query_device over in-process ranks (device tensors through
     the communicator), global tier built with the device kernels."""
