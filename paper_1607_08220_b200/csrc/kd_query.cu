@@ -344,7 +344,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
               const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
               const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
               int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter,
-              bool push_free_first) {
+              bool push_free_first, const uint32_t* __restrict__ home_keys) {
     constexpr int DC = Dims<DT>::cap;
     constexpr int POOL = 64;
     const int D = DT > 0 ? DT : dims_rt;
@@ -458,7 +458,9 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 first = push_free_first;
 #pragma unroll
                 for (int d = 0; d < DC; d++) off[d] = 0.0f;
-                node = n_nodes > 0 ? 0 : -2;  // -2: finished immediately (empty tree)
+                // -2: finished immediately (empty tree).  With the home-leaf sort keys the
+                // first (push-free) descent is a jump: k_leaf_of already walked it.
+                node = n_nodes > 0 ? ((home_keys && first) ? (int)home_keys[myq] : 0) : -2;
             }
         }
         if (node == -2) {
@@ -889,7 +891,7 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
             k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
                 t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
-                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, knn_push_free_first());
+                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, knn_push_free_first(), home);
             cudaFreeAsync(ctr, st);
             return;
         }
