@@ -621,14 +621,14 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
 constexpr int WQ_WARPS = 4;
 constexpr int WQ_DC = 16;  // max dimensions
 
-template <typename T, int KM>
+template <typename T, int KM, int DCAP>
 __global__ void __launch_bounds__(WQ_WARPS * 32)
 k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
          const uint64_t* __restrict__ ids, int64_t n, int D, const double* __restrict__ queries,
          const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
          const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
          int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
-    constexpr int DC = WQ_DC;
+    constexpr int DC = DCAP;  // register arrays sized for the dimension count (10 for C4, else 16)
     __shared__ int s_node[WQ_WARPS][QCAP];
     __shared__ float s_off[WQ_WARPS][QCAP][32];
     __shared__ double s_q[WQ_WARPS][DC];
@@ -709,52 +709,60 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                 node = near;
                 continue;
             }
-            // bucket: one point per lane per round
+            // bucket: one point per lane per round, two rounds' loads issued together
             const int start = rec.a, len = -1 - rec.db;
             c1++;
             c2 += len;
-            for (int c = 0; c < len; c += 32) {
-                const int j = c + lane;
-                const bool valid = j < len;
-                T cv[DC];
+            for (int c = 0; c < len; c += 64) {
+                T cv[2][DC];
 #pragma unroll
-                for (int d = 0; d < DC; d++)
-                    if (d < D) cv[d] = valid ? coords[(int64_t)d * n + start + j] : T(0);
-                bool pass = valid;
-                if constexpr (sizeof(T) == 4) {
-                    float d32 = 0.0f;
+                for (int h = 0; h < 2; h++) {
+                    const int j = c + h * 32 + lane;
 #pragma unroll
-                    for (int d = 0; d < DC; d++) {
-                        if (d < D) {
-                            const float tt = cv[d] - q32[d];
-                            d32 = fmaf(tt, tt, d32);
-                        }
-                    }
-                    pass = pass && !(d32 > thr32);
+                    for (int d = 0; d < DC; d++)
+                        if (d < D) cv[h][d] = j < len ? coords[(int64_t)d * n + start + j] : T(0);
                 }
-                double dist = INFINITY;
-                if (pass) {
-                    dist = 0.0;
 #pragma unroll
-                    for (int d = 0; d < DC; d++) {
-                        if (d < D) {
-                            const double df = __dsub_rn((double)cv[d], s_q[warp][d]);
-                            dist = __dadd_rn(dist, __dmul_rn(df, df));
+                for (int h = 0; h < 2; h++) {
+                    const int cc = c + h * 32;
+                    if (cc >= len) break;
+                    const bool valid = cc + lane < len;
+                    bool pass = valid;
+                    if constexpr (sizeof(T) == 4) {
+                        float d32 = 0.0f;
+#pragma unroll
+                        for (int d = 0; d < DC; d++) {
+                            if (d < D) {
+                                const float tt = cv[h][d] - q32[d];
+                                d32 = fmaf(tt, tt, d32);
+                            }
                         }
+                        pass = pass && !(d32 > thr32);
                     }
-                    pass = cnt < kk ? dist < radius : dist <= kth_d;
-                }
-                unsigned m = __ballot_sync(FULL, pass);
-                while (m) {  // survivors in point order, inserted uniformly by every lane
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const double dd = __shfl_sync(FULL, dist, src);
-                    const uint32_t pos = (uint32_t)(start + c + src);
-                    if (cnt < kk ? dd < radius : (dd <= kth_d && lexless_pos(dd, pos, kth_d, kth_p, ids))) {
-                        topk_insert_pos<KM>(bd, bp, cnt, kk, dd, pos, ids);
-                        if (cnt == kk) {
-                            topk_last<KM>(bd, bp, kk, kth_d, kth_p);
-                            if constexpr (sizeof(T) == 4) thr32 = make_thr(kth_d);
+                    double dist = INFINITY;
+                    if (pass) {
+                        dist = 0.0;
+#pragma unroll
+                        for (int d = 0; d < DC; d++) {
+                            if (d < D) {
+                                const double df = __dsub_rn((double)cv[h][d], s_q[warp][d]);
+                                dist = __dadd_rn(dist, __dmul_rn(df, df));
+                            }
+                        }
+                        pass = cnt < kk ? dist < radius : dist <= kth_d;
+                    }
+                    unsigned m = __ballot_sync(FULL, pass);
+                    while (m) {  // survivors in point order, inserted uniformly by every lane
+                        const int src = __ffs(m) - 1;
+                        m &= m - 1;
+                        const double dd = __shfl_sync(FULL, dist, src);
+                        const uint32_t pos = (uint32_t)(start + cc + src);
+                        if (cnt < kk ? dd < radius : (dd <= kth_d && lexless_pos(dd, pos, kth_d, kth_p, ids))) {
+                            topk_insert_pos<KM>(bd, bp, cnt, kk, dd, pos, ids);
+                            if (cnt == kk) {
+                                topk_last<KM>(bd, bp, kk, kth_d, kth_p);
+                                if constexpr (sizeof(T) == 4) thr32 = make_thr(kth_d);
+                            }
                         }
                     }
                 }
@@ -862,19 +870,24 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
     const unsigned blocks = (unsigned)((a.nq + threads - 1) / threads);
     if constexpr (KM > 0 && DT == 0) {
         if (!a.thread_per_query && t.dims <= WQ_DC) {
-            int dev = 0, sms = 148, per_sm = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_wq<T, KM>, WQ_WARPS * 32, 0);
-            const long long want = (a.nq + WQ_WARPS - 1) / WQ_WARPS;
-            const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
-            unsigned long long* ctr = nullptr;
-            KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
-            KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-            k_knn_wq<T, KM><<<grid, WQ_WARPS * 32, 0, st>>>(
-                t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
-                (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
-            cudaFreeAsync(ctr, st);
+            auto go = [&](auto kern) {
+                int dev = 0, sms = 148, per_sm = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WQ_WARPS * 32, 0);
+                const long long want = (a.nq + WQ_WARPS - 1) / WQ_WARPS;
+                const unsigned grid =
+                    (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
+                unsigned long long* ctr = nullptr;
+                KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
+                KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+                kern<<<grid, WQ_WARPS * 32, 0, st>>>(t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n,
+                                                     t.dims, a.queries, order, a.nq, (int)a.k, a.radii, a.excl,
+                                                     a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
+                cudaFreeAsync(ctr, st);
+            };
+            if (t.dims <= 10) go(k_knn_wq<T, KM, 10>);
+            else go(k_knn_wq<T, KM, WQ_DC>);
             return;
         }
     }
