@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -347,7 +348,11 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         new (&bi) DevBuf(nq * k * 8, st);
         new (&bc) DevBuf(nq * 8, st);
         if (out_ctr) new (&bctr) DevBuf(nq * 3 * 8, st);
-        const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(KNN_MAX_CHUNKS, nq / KNN_CHUNK_MIN));
+        static const int64_t max_chunks = [] {  // KDB_KNN_CHUNKS overrides (A/B measurements)
+            const char* e = std::getenv("KDB_KNN_CHUNKS");
+            return e ? std::max<int64_t>(1, atoll(e)) : KNN_MAX_CHUNKS;
+        }();
+        const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(max_chunks, nq / KNN_CHUNK_MIN));
         const int64_t csz = (nq + nch - 1) / nch;
         cudaStream_t s_in = nullptr, s_out = nullptr;
         KD_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
