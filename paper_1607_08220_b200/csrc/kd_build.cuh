@@ -1722,14 +1722,6 @@ static __global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const i
     if (i < n) ids_out[i] = ids_in ? ids_in[perm[i]] : (uint64_t)perm[i];
 }
 
-template <typename T>
-__global__ void k_init(const T* __restrict__ in, T* __restrict__ buf, int32_t* __restrict__ idx, int64_t n, int D) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    for (int d = 0; d < D; d++) buf[(int64_t)d * n + i] = in[(int64_t)d * n + i];
-    idx[i] = (int32_t)i;
-}
-
 static __global__ void k_count_leaves(const KdNode* nodes, int64_t nn, unsigned long long* out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool leaf = i < nn && nodes[i].db < 0;

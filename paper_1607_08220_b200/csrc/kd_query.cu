@@ -37,32 +37,6 @@ __device__ __forceinline__ bool lexless(double d0, uint64_t i0, double d1, uint6
     return d0 < d1 || (d0 == d1 && i0 < i1);
 }
 
-// insert (d, id) into the ascending list (bd, bi)[0 .. cnt) of capacity k <= KM,
-// dropping the last entry when full (the caller has checked that it enters):
-// one descending pass, each slot either keeps, shifts from its predecessor, or
-// takes the new entry.
-template <int KM>
-__device__ __forceinline__ void topk_insert(double (&bd)[KM], uint64_t (&bi)[KM], int& cnt, int k, double d,
-                                            uint64_t id) {
-    const int last = cnt < k ? cnt : k - 1;  // slot that receives a value
-    bool placed = false;
-#pragma unroll
-    for (int jj = KM - 1; jj >= 0; jj--) {
-        if (jj <= last && !placed) {
-            const bool shift = jj > 0 && lexless(d, id, bd[jj > 0 ? jj - 1 : 0], bi[jj > 0 ? jj - 1 : 0]);
-            if (shift) {
-                bd[jj] = bd[jj > 0 ? jj - 1 : 0];
-                bi[jj] = bi[jj > 0 ? jj - 1 : 0];
-            } else {
-                bd[jj] = d;
-                bi[jj] = id;
-                placed = true;
-            }
-        }
-    }
-    if (cnt < k) cnt++;
-}
-
 // same list keyed by (sq_dist, packed row): ids are only read to break exact
 // distance ties (lexicographic (d, id) order is preserved exactly)
 __device__ __forceinline__ bool lexless_pos(double d0, uint32_t p0, double d1, uint32_t p1,
