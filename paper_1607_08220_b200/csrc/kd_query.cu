@@ -914,6 +914,77 @@ static void dispatch_d(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
     else dispatch_k<T, 0>(t, a, order, home, st);
 }
 
+// Z-order (Morton) keys of 3-D queries over their bounding box, 10 bits per
+// dimension: a traversal-free spatial order for the persistent kernel (which then
+// walks the first descent itself).  KDB_KNN_ORDER=leaf selects the home-leaf order.
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ord_inv(unsigned long long k) {
+    const unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+static __global__ void k_qbox(const double* __restrict__ q, int64_t nq, unsigned long long* __restrict__ box) {
+    unsigned long long lo[3] = {~0ULL, ~0ULL, ~0ULL}, hi[3] = {0ULL, 0ULL, 0ULL};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            const unsigned long long k = ord_key(q[i * 3 + d]);
+            lo[d] = k < lo[d] ? k : lo[d];
+            hi[d] = k > hi[d] ? k : hi[d];
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xFFFFFFFFu, lo[d], o), b = __shfl_xor_sync(0xFFFFFFFFu, hi[d], o);
+            lo[d] = a < lo[d] ? a : lo[d];
+            hi[d] = b > hi[d] ? b : hi[d];
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&box[d], lo[d]);
+            atomicMax(&box[3 + d], hi[d]);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t spread11(uint32_t x) {  // 11 bits -> every third bit of 33
+    uint64_t v = x & 0x7FF;
+    v = (v | (v << 16)) & 0x1F0000FFULL;
+    v = (v | (v << 8)) & 0x100F00F00FULL;
+    v = (v | (v << 4)) & 0x10C30C30C3ULL;
+    v = (v | (v << 2)) & 0x1249249249ULL;
+    return (uint32_t)v;  // bits >= 32 dropped by the callers' shifts
+}
+
+static __global__ void k_morton(const double* __restrict__ q, int64_t nq, const unsigned long long* __restrict__ box,
+                                uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    uint32_t c[3];
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        const double lo = ord_inv(box[d]), hi = ord_inv(box[3 + d]);
+        const double w = hi > lo ? 2047.999 / (hi - lo) : 0.0;
+        const double u = (q[i * 3 + d] - lo) * w;
+        c[d] = (uint32_t)fmin(fmax(u, 0.0), 2047.0);
+    }
+    // 32-bit key: x and y with 11 bits, z with 10 (its lowest bit dropped)
+    const uint64_t k = ((uint64_t)spread11(c[0]) << 2) | ((uint64_t)spread11(c[1]) << 1) | (uint64_t)spread11(c[2]);
+    key[i] = (uint32_t)(k >> 1);
+    val[i] = (int32_t)i;
+}
+
+static bool knn_morton_order() {
+    static const bool v = [] {
+        const char* e = getenv("KDB_KNN_ORDER");
+        return !(e && e[0] == 'l');
+    }();
+    return v;
+}
+
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
     if (a.nq == 0) return;
     int32_t* order = nullptr;
@@ -925,18 +996,32 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
         KD_CUDA(cudaMallocAsync((void**)&k1, a.nq * 4, st));
         KD_CUDA(cudaMallocAsync((void**)&v0, a.nq * 4, st));
         KD_CUDA(cudaMallocAsync((void**)&order, a.nq * 4, st));
-        const unsigned blocks = (unsigned)((a.nq + 1023) / 1024);  // 4 queries per thread
-        if (t.dims == 3) k_leaf_of<3><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
-        else k_leaf_of<0><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
+        const bool morton = t.dims == 3 && knn_morton_order();
         int bits = 1;
-        while (bits < 32 && ((int64_t)1 << bits) < t.n_nodes) bits++;
+        if (morton) {
+            unsigned long long* box = nullptr;
+            KD_CUDA(cudaMallocAsync((void**)&box, 6 * sizeof(unsigned long long), st));
+            const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
+            KD_CUDA(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, st));
+            k_qbox<<<592, 256, 0, st>>>(a.queries, a.nq, box);
+            k_morton<<<(unsigned)((a.nq + 255) / 256), 256, 0, st>>>(a.queries, a.nq, box, k0, v0);
+            cudaFreeAsync(box, st);
+            bits = 32;
+        } else {
+            const unsigned blocks = (unsigned)((a.nq + 1023) / 1024);  // 4 queries per thread
+            if (t.dims == 3) k_leaf_of<3><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
+            else k_leaf_of<0><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
+            while (bits < 32 && ((int64_t)1 << bits) < t.n_nodes) bits++;
+        }
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
         KD_CUDA(cudaMallocAsync(&tmp, tb, st));
         cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
     }
-    if (t.dtype == DT_F32) dispatch_d<float>(t, a, order, order ? k1 : nullptr, st);
-    else dispatch_d<double>(t, a, order, order ? k1 : nullptr, st);
+    // the persistent kernel may jump straight to the home leaf only with home-leaf keys
+    const uint32_t* home = (order && !(t.dims == 3 && knn_morton_order())) ? k1 : nullptr;
+    if (t.dtype == DT_F32) dispatch_d<float>(t, a, order, home, st);
+    else dispatch_d<double>(t, a, order, home, st);
     KD_CUDA(cudaGetLastError());
     if (order) {
         cudaFreeAsync(k0, st); cudaFreeAsync(k1, st); cudaFreeAsync(v0, st); cudaFreeAsync(order, st);
