@@ -1305,7 +1305,7 @@ __device__ __forceinline__ bool closer_to_half(int64_t b, int64_t a, int64_t n) 
 // dimension's keys are sorted by the unrolled network (warp_sort_t) instead of
 // radix-select passes.  Same decisions as sub_split (same certified bound).
 template <typename T, int DT, int SR>
-__device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm, int n, int ts, uint64_t path,
+__device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, int n, int ts, uint64_t path,
                                                 const DevCtx& c, uint32_t* fyslots, int* fylocks, int& out_dim,
                                                 double& out_val, int& out_nl) {
     typedef typename KeyOf<T>::type Key;
@@ -1419,7 +1419,7 @@ __device__ __forceinline__ void sub_split_small(const T* cs, const uint16_t* pm,
 }
 
 template <typename T, int DT>
-__device__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int dims_rt, uint64_t path,
+__device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, int ts, int dims_rt, uint64_t path,
                           const DevCtx& c, uint32_t* hist, uint32_t* fyslots, int* fylocks, int& out_dim,
                           double& out_val, int& out_nl) {
     typedef typename KeyOf<T>::type Key;
