@@ -136,7 +136,7 @@ __device__ __forceinline__ uint64_t mod_u64_u32(uint64_t z, uint32_t d) {
 // that targets t -- turns each chain hop into one or two shared loads instead of
 // a binary search.
 template <int R, typename K>
-__device__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t* picked, uint16_t* gidx = nullptr) {
+__device__ __noinline__ void fy_resolve(uint32_t n, int m, uint64_t seed, K* skeys, uint32_t* picked, uint16_t* gidx = nullptr) {
     const int lane = threadIdx.x & 31;
     K v[R];
 #pragma unroll
@@ -231,7 +231,7 @@ constexpr int FYD_MAX = 4096;
 constexpr uint16_t FYD_NONE = 0xFFFF;
 
 template <int R>
-__device__ void fy_direct(uint32_t n, int m, uint64_t seed, uint16_t* last, uint16_t* back, uint32_t* picked) {
+__device__ __noinline__ void fy_direct(uint32_t n, int m, uint64_t seed, uint16_t* last, uint16_t* back, uint32_t* picked) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1;
     for (uint32_t i = lane; i < (n + 1) / 2; i += 32) reinterpret_cast<uint32_t*>(last)[i] = 0xFFFFFFFFu;
