@@ -30,7 +30,7 @@ T = 'gpu__time_duration.sum'
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 build_b = query_b = 0.0
 build_t = query_t = 0.0
-first_query = [i for i in range(start, end + 1) if 'k_leaf_of' in seq[i]['name']]
+first_query = [i for i in range(start, end + 1) if any(q in seq[i]['name'] for q in ('k_leaf_of', 'k_qbox', 'k_morton'))]
 qstart = first_query[0] if first_query else end
 for i, e in enumerate(seq[start:end + 1], start):
     short = e['name'].split('(')[0].replace('void ', '')[:70]
