@@ -656,34 +656,51 @@ k_hist(const T* __restrict__ src, const TileInfo* __restrict__ tinfo, uint32_t t
     if (threadIdx.x == 0 && nL) atomicAdd(&split[cur_ni].L, nL);
 }
 
+// everything the scatter needs about one half-tile, written by k_tile_left so the
+// scatter's per-half-tile setup is one record load (+ the two scan entries)
+struct HalfMeta {
+    int64_t gbase;  // node start
+    double value;   // split value
+    int64_t nl;     // node's left count
+    int32_t e0, e1; // element range within the node (e1 <= e0: nothing to move)
+    int32_t dim;
+    uint32_t first_hb;  // the node's first half-tile
+};
+
 // per half-tile count of elements going left: L_h + sum of the window bins
 // below the chosen boundary (warp per half-tile); nodes split by the slow path
 // (value not a window boundary) count from the data
 template <typename T>
 __global__ void k_tile_left(const T* __restrict__ src, const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap,
                             DevCtx c, const Split* __restrict__ split, const uint16_t* __restrict__ hrow,
-                            const uint32_t* __restrict__ hL, uint32_t nhalf, uint32_t* __restrict__ tile_left) {
+                            const uint32_t* __restrict__ hL, uint32_t nhalf, uint32_t* __restrict__ tile_left,
+                            HalfMeta* __restrict__ meta) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t hb = blockIdx.x * (blockDim.x >> 5) + warp;
     if (hb >= nhalf) return;
     const uint32_t t = hb / SUB, sub = hb % SUB;
     const int ni = tmap[t];
     const Split sp = split[ni];
+    const LNode nd = nodes[ni];
+    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
+    const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
     uint32_t cnt = 0;
     if (sp.status == ST_SPLIT) {
         if (sp.wsel >= 0) {
             for (int i = 1 + lane; i <= sp.wsel; i += 32) cnt += hrow[(size_t)hb * WIN + i];
             cnt = warp_isum(cnt) + hL[hb];
         } else {
-            const LNode nd = nodes[ni];
-            const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
-            const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
             const T* row = src + (int64_t)sp.dim * c.N + nd.start;
             for (int64_t e = e0 + lane; e < e1; e += 32) cnt += (double)row[e] < sp.value;
             cnt = warp_isum(cnt);
         }
     }
-    if (lane == 0) tile_left[hb] = cnt;
+    if (lane == 0) {
+        tile_left[hb] = cnt;
+        const bool moves = sp.status == ST_SPLIT && e0 < e1;
+        meta[hb] = HalfMeta{nd.start, sp.value, sp.nl, (int32_t)e0, moves ? (int32_t)e1 : (int32_t)e0, sp.dim,
+                            nd.tile_off * SUB};
+    }
 }
 
 // ============================================================================
@@ -978,8 +995,8 @@ k_slow(const T* __restrict__ src, const LNode* __restrict__ nodes, DevCtx c, Spl
 template <typename T, int DT, int CH>
 __global__ void __launch_bounds__(TILE_THREADS)
 k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
-          int32_t* __restrict__ idst, const LNode* __restrict__ nodes, const TileInfo* __restrict__ tinfo, DevCtx c,
-          const Split* __restrict__ split, const uint32_t* __restrict__ tile_loff, uint32_t nhalf) {
+          int32_t* __restrict__ idst, const HalfMeta* __restrict__ meta, DevCtx c,
+          const uint32_t* __restrict__ tile_loff, uint32_t nhalf) {
     constexpr int NW = TILE_THREADS / 32;
     constexpr int DC = DT > 0 ? DT : 16;
     __shared__ uint32_t wl[CH * NW];
@@ -989,21 +1006,15 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
     // persistent: a grid of resident CTAs strides over the half-tiles (empty second
     // halves of small nodes cost a loop iteration, not a CTA launch)
     for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x) {
-    const uint32_t t = hb / SUB, sub = hb % SUB;
-    const TileInfo ti = tinfo[t];
-    if ((int)sub * (TILE / SUB) >= ti.cnt) continue;  // empty second half of a small node: one load
-    const int ni = ti.ni;
-    const LNode nd = nodes[ni];
-    const Split sp = split[ni];
-    if (sp.status != ST_SPLIT) continue;
-    const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE + (int64_t)sub * (TILE / SUB);
-    const int64_t e1 = min((int64_t)nd.n, e0 + TILE / SUB);
-    if (e0 >= e1) continue;
-    const uint32_t lbefore = tile_loff[hb] - tile_loff[nd.tile_off * SUB];  // lefts earlier in this node
+    const HalfMeta hm = meta[hb];
+    if (hm.e1 <= hm.e0) continue;  // not split, or the empty second half of a small node
+    const int64_t e0 = hm.e0, e1 = hm.e1;
+    struct { int dim; double value; int64_t nl; } sp{hm.dim, hm.value, hm.nl};
+    const uint32_t lbefore = tile_loff[hb] - tile_loff[hm.first_hb];  // lefts earlier in this node
     int64_t lrun = lbefore;
     int64_t rrun = e0 - lbefore;
     const int64_t N = c.N;
-    const int64_t gbase = nd.start;
+    const int64_t gbase = hm.gbase;
     for (int64_t pass = e0; pass < e1; pass += (int64_t)CH * TILE_THREADS) {
         T x[CH][DC];
         int32_t id[CH];
@@ -1971,14 +1982,16 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
                                                                                   hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
-        k_tile_left<T><<<(tiles * SUB + 7) / 8, 256, 0, st>>>(lsrc, lv, tmap, c, split, hrow, hL, tiles * SUB, tile_left);
+        HalfMeta* hmeta = dalloc<HalfMeta>((size_t)tiles * SUB, st);
+        k_tile_left<T><<<(tiles * SUB + 7) / 8, 256, 0, st>>>(lsrc, lv, tmap, c, split, hrow, hL, tiles * SUB, tile_left,
+                                                                hmeta);
         size_t tmp_bytes = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
         void* tmp = dalloc<unsigned char>(tmp_bytes, st);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
 #define KD_SCATTER(DTV, CHV)                                                                                   \
     k_scatter<T, DTV, CHV><<<std::min<uint32_t>(tiles * SUB, scatter_grid), TILE_THREADS, 0, st>>>(                  \
-        lsrc, lidx, buf[1 - par], idx[1 - par], lv, tinfo, c, split, tile_loff, tiles * SUB)
+        lsrc, lidx, buf[1 - par], idx[1 - par], hmeta, c, tile_loff, tiles * SUB)
         switch (dims) {
             case 1: KD_SCATTER(1, 8); break;
             case 2: KD_SCATTER(2, 8); break;
@@ -2001,7 +2014,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         tr.mark("level done", (int)levels.size());
         slow_total += *h_slow;
         ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
-        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st);
+        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st); dfree(hmeta, st);
         dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
