@@ -491,11 +491,6 @@ __device__ __forceinline__ int tile_node(const LNode* nodes, int K, uint32_t t) 
     return lo;
 }
 
-// tile -> node of the level (once per level, so the tile kernels start with one load)
-static __global__ void k_tile_map(const LNode* __restrict__ nodes, int K, uint32_t tiles, int32_t* __restrict__ tmap) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < tiles) tmap[t] = tile_node(nodes, K, t);
-}
 
 // ============================================================================
 // k_hist: windowed histogram (median.py:128-140 restricted to the boundaries
@@ -521,12 +516,13 @@ struct TileInfo {
     int64_t off;
 };
 
-static __global__ void k_tile_info(const LNode* __restrict__ nodes, const int32_t* __restrict__ tmap,
+static __global__ void k_tile_info(const LNode* __restrict__ nodes, int K, int32_t* __restrict__ tmap,
                                    const Split* __restrict__ split, uint32_t tiles, int64_t N,
                                    TileInfo* __restrict__ tinfo) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= tiles) return;
-    const int ni = tmap[t];
+    const int ni = tile_node(nodes, K, t);
+    tmap[t] = ni;
     const LNode nd = nodes[ni];
     const int64_t e0 = (int64_t)(t - nd.tile_off) * TILE;
     const int64_t e1 = min((int64_t)nd.n, e0 + TILE);
@@ -1866,10 +1862,15 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     // tasks: at most one per point range; bounded by 2 * (#top nodes) + 1 -> grow with the store
     size_t task_cap = 1024;
     Task* tasks = dalloc<Task>(task_cap, st);
-    int* task_ctr = dalloc<int>(1, st);
-    KD_CUDA(cudaMemsetAsync(task_ctr, 0, sizeof(int), st));
-    unsigned long long* next_ctr = dalloc<unsigned long long>(2, st);  // [0] packed count/tiles, [1] max child size
-    int* slow_count = dalloc<int>(1, st);
+    // level counters in one block (one clear and one read-back per level):
+    //   [0] next level's packed (node count << 32 | tiles), [1] max child size (low) | slow nodes (high),
+    //   [2] subtree task count (cumulative over levels)
+    unsigned long long* ctr = dalloc<unsigned long long>(3, st);
+    KD_CUDA(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), st));
+    unsigned long long* next_ctr = ctr;
+    int* next_max = reinterpret_cast<int*>(ctr + 1);
+    int* slow_count = next_max + 1;
+    int* task_ctr = reinterpret_cast<int*>(ctr + 2);
     unsigned long long* h_ctr = nullptr;
     h_ctr = pinned_counters(out->device);
 
@@ -1958,7 +1959,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         int* slow_list = dalloc<int>(K, st);
         uint32_t* tile_left = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
         uint32_t* tile_loff = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
-        KD_CUDA(cudaMemsetAsync(slow_count, 0, sizeof(int), st));
+        KD_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));  // next, max child, slow nodes
         if (K <= sample_cta_max) {
             if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
             else k_sample_cta<T, 0><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
@@ -1973,11 +1974,10 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
             }
         }
         int32_t* tmap = dalloc<int32_t>(tiles, st);
-        k_tile_map<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tiles, tmap);
         uint16_t* hrow = dalloc<uint16_t>((size_t)tiles * SUB * WIN, st);
         uint32_t* hL = dalloc<uint32_t>((size_t)tiles * SUB, st);
         TileInfo* tinfo = dalloc<TileInfo>(tiles, st);
-        k_tile_info<<<(tiles + 255) / 256, 256, 0, st>>>(lv, tmap, split, tiles, c.N, tinfo);
+        k_tile_info<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tmap, split, tiles, c.N, tinfo);
         k_hist<T><<<std::min<uint32_t>(tiles, hist_grid), TILE_THREADS, 2 * TILE * sizeof(T), st>>>(lsrc, tinfo, tiles, split, wb, wf, hrow,
                                                                                   hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
@@ -2001,26 +2001,21 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         }
 #undef KD_SCATTER
         LNode* next = dalloc<LNode>(2 * (size_t)K, st);
-        KD_CUDA(cudaMemsetAsync(next_ctr, 0, sizeof(unsigned long long) + sizeof(int), st));
         k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, at_input ? 2 : par, (int)ts_used, ts, next, next_ctr,
-                                                    tasks, task_ctr, reinterpret_cast<int*>(next_ctr + 1));
+                                                    tasks, task_ctr, next_max);
         KD_CUDA(cudaGetLastError());
-        KD_CUDA(cudaMemcpyAsync(&h_ctr[0], next_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        KD_CUDA(cudaMemcpyAsync(&h_ctr[1], task_ctr, sizeof(int), cudaMemcpyDeviceToHost, st));
-        int* h_slow = reinterpret_cast<int*>(&h_ctr[1]) + 1;
-        KD_CUDA(cudaMemcpyAsync(h_slow, slow_count, sizeof(int), cudaMemcpyDeviceToHost, st));
-        KD_CUDA(cudaMemcpyAsync(&h_ctr[2], next_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KD_CUDA(cudaMemcpyAsync(h_ctr, ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         KD_CUDA(cudaStreamSynchronize(st));
         tr.mark("level done", (int)levels.size());
-        slow_total += *h_slow;
-        ntasks_known = (int)(h_ctr[1] & 0xFFFFFFFFULL);
+        slow_total += (int)(h_ctr[1] >> 32);
+        ntasks_known = (int)(h_ctr[2] & 0xFFFFFFFFULL);
         dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st); dfree(hmeta, st);
         dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
         K = (int)(h_ctr[0] >> 32);
         tiles = (uint32_t)(h_ctr[0] & 0xFFFFFFFFULL);
-        max_node = (int64_t)(int32_t)(h_ctr[2] & 0xFFFFFFFFULL);
+        max_node = (int64_t)(int32_t)(h_ctr[1] & 0xFFFFFFFFULL);
         par = 1 - par;
         at_input = false;
         if (K > 0) levels.push_back(next);
@@ -2103,7 +2098,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     dfree(buf[1], st); dfree(idx[1], st);
     for (auto l : levels) dfree(l, st);
     ts_free(ts);
-    dfree(tasks, st); dfree(task_ctr, st); dfree(next_ctr, st); dfree(slow_count, st);
+    dfree(tasks, st); dfree(ctr, st);
     dfree(scratch, st); dfree(scnt, st); dfree(sstack, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
     dfree(d_leaves, st);
     cudaEventDestroy(e0);
