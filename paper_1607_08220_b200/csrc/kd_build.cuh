@@ -1928,8 +1928,27 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int64_t slow_total = 0;
     int64_t max_node = n;  // largest node of the current level (read back with the level counters)
     bool at_input = true;  // the first level reads the caller's points directly (row ids = positions)
+    // per-level scratch, allocated once at bounds that hold for every level: a level's
+    // nodes all exceed ts points, so K <= n / (ts + 1) + 1, and its tiles <= n / TILE + K
+    const size_t kmax = (size_t)(n / (c.ts + 1)) + 2;
+    const size_t tmax = (size_t)(n / TILE) + kmax + 1;
+    Split* split = dalloc<Split>(kmax, st);
+    T* wb = dalloc<T>(kmax * WIN, st);
+    uint32_t* wf = dalloc<uint32_t>(kmax * WIN, st);
+    int* slow_list = dalloc<int>(kmax, st);
+    uint32_t* tile_left = dalloc<uint32_t>(tmax * SUB + 1, st);
+    uint32_t* tile_loff = dalloc<uint32_t>(tmax * SUB + 1, st);
+    int32_t* tmap = dalloc<int32_t>(tmax, st);
+    uint16_t* hrow = dalloc<uint16_t>(tmax * SUB * WIN, st);
+    uint32_t* hL = dalloc<uint32_t>(tmax * SUB, st);
+    TileInfo* tinfo = dalloc<TileInfo>(tmax, st);
+    HalfMeta* hmeta = dalloc<HalfMeta>(tmax * SUB, st);
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tile_left, tile_loff, (int)(tmax * SUB), st);
+    void* scan_tmp = dalloc<unsigned char>(scan_bytes, st);
     while (K > 0) {
         LNode* lv = levels.back();
+        if ((size_t)K > kmax || (size_t)tiles > tmax) throw CudaError{"level exceeds the preallocated bounds"};
         const T* lsrc = at_input ? d_in : buf[par];
         const int32_t* lidx = at_input ? nullptr : idx[par];
         const bool big_levels = max_node > (int64_t(1) << 22);
@@ -1953,12 +1972,6 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
             tasks = t2;
             task_cap = nc;
         }
-        Split* split = dalloc<Split>(K, st);
-        T* wb = dalloc<T>((size_t)K * WIN, st);
-        uint32_t* wf = dalloc<uint32_t>((size_t)K * WIN, st);
-        int* slow_list = dalloc<int>(K, st);
-        uint32_t* tile_left = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
-        uint32_t* tile_loff = dalloc<uint32_t>((size_t)tiles * SUB + 1, st);
         KD_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));  // next, max child, slow nodes
         if (K <= sample_cta_max) {
             if (dims == 3) k_sample_cta<T, 3><<<K, CTA_S, 0, st>>>(lsrc, lv, c, split, wb, wf);
@@ -1973,22 +1986,23 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
                 if (big_levels) k_sample<T, 0, true><<<sg, SAMPLE_WARPS * 32, sample_smem64, st>>>(lsrc, lv, K, c, split, wb, wf);
             }
         }
-        int32_t* tmap = dalloc<int32_t>(tiles, st);
-        uint16_t* hrow = dalloc<uint16_t>((size_t)tiles * SUB * WIN, st);
-        uint32_t* hL = dalloc<uint32_t>((size_t)tiles * SUB, st);
-        TileInfo* tinfo = dalloc<TileInfo>(tiles, st);
         k_tile_info<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tmap, split, tiles, c.N, tinfo);
         k_hist<T><<<std::min<uint32_t>(tiles, hist_grid), TILE_THREADS, 2 * TILE * sizeof(T), st>>>(lsrc, tinfo, tiles, split, wb, wf, hrow,
                                                                                   hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
-        HalfMeta* hmeta = dalloc<HalfMeta>((size_t)tiles * SUB, st);
         k_tile_left<T><<<(tiles * SUB + 7) / 8, 256, 0, st>>>(lsrc, lv, tmap, c, split, hrow, hL, tiles * SUB, tile_left,
                                                                 hmeta);
-        size_t tmp_bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
-        void* tmp = dalloc<unsigned char>(tmp_bytes, st);
-        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
+        {
+            size_t need = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, need, tile_left, tile_loff, (int)(tiles * SUB), st);
+            if (need > scan_bytes) {
+                dfree(scan_tmp, st);
+                scan_tmp = dalloc<unsigned char>(need, st);
+                scan_bytes = need;
+            }
+            cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, tile_left, tile_loff, (int)(tiles * SUB), st);
+        }
 #define KD_SCATTER(DTV, CHV)                                                                                   \
     k_scatter<T, DTV, CHV><<<std::min<uint32_t>(tiles * SUB, scatter_grid), TILE_THREADS, 0, st>>>(                  \
         lsrc, lidx, buf[1 - par], idx[1 - par], hmeta, c, tile_loff, tiles * SUB)
@@ -2009,8 +2023,6 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         tr.mark("level done", (int)levels.size());
         slow_total += (int)(h_ctr[1] >> 32);
         ntasks_known = (int)(h_ctr[2] & 0xFFFFFFFFULL);
-        dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st); dfree(hmeta, st);
-        dfree(tile_loff, st); dfree(tmp, st); dfree(tmap, st);
         level_k.push_back(K);
         ts_used += 2 * (size_t)K;
         K = (int)(h_ctr[0] >> 32);
@@ -2021,6 +2033,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         if (K > 0) levels.push_back(next);
         else dfree(next, st);
     }
+    dfree(split, st); dfree(wb, st); dfree(wf, st); dfree(slow_list, st); dfree(tile_left, st); dfree(tile_loff, st);
+    dfree(tmap, st); dfree(hrow, st); dfree(hL, st); dfree(tinfo, st); dfree(hmeta, st); dfree(scan_tmp, st);
     tr.mark("top phase done");
     const int ntasks = ntasks_known > 0 ? ntasks_known : 1;
     // subtree phase
