@@ -1729,12 +1729,6 @@ static __global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const i
     if (i < n) ids_out[i] = ids_in ? ids_in[perm[i]] : (uint64_t)perm[i];
 }
 
-static __global__ void k_count_leaves(const KdNode* nodes, int64_t nn, unsigned long long* out) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool leaf = i < nn && nodes[i].db < 0;
-    const unsigned b = __ballot_sync(FULL, leaf);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
-}
 
 // ============================================================================
 // host orchestration
@@ -2078,22 +2072,17 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     k_relocate<<<ntasks, 256, 0, st>>>(tasks, task_nodes, task_base, scratch, scnt, nodes, ncount);
     uint64_t* ids_out = dalloc<uint64_t>(n, st);
     k_gather_ids<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_ids, idx[0], ids_out, n);
-    unsigned long long* d_leaves = dalloc<unsigned long long>(1, st);
-    KD_CUDA(cudaMemsetAsync(d_leaves, 0, sizeof(unsigned long long), st));
-    k_count_leaves<<<(unsigned)((total_nodes + 255) / 256), 256, 0, st>>>(nodes, total_nodes, d_leaves);
     KD_CUDA(cudaGetLastError());
     // depth = max(task depths, top levels)
     std::vector<int32_t> hdepth(ntasks);
     KD_CUDA(cudaMemcpyAsync(hdepth.data(), task_depth, sizeof(int32_t) * ntasks, cudaMemcpyDeviceToHost, st));
-    unsigned long long hleaves = 0;
-    KD_CUDA(cudaMemcpyAsync(&hleaves, d_leaves, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     KD_CUDA(cudaEventRecord(e1, st));
     KD_CUDA(cudaStreamSynchronize(st));
     tr.mark("finalize done");
     int64_t depth = 0;
     for (int i = 0; i < ntasks_known; i++) depth = std::max<int64_t>(depth, hdepth[i]);
     out->n_nodes = total_nodes;
-    out->n_leaves = (int64_t)hleaves;
+    out->n_leaves = ((int64_t)total_nodes + 1) / 2;  // full binary tree: every interior node has two children
     out->depth = depth;
     out->nodes = nodes;
     out->node_count = ncount;
@@ -2114,7 +2103,6 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     ts_free(ts);
     dfree(tasks, st); dfree(ctr, st);
     dfree(scratch, st); dfree(scnt, st); dfree(sstack, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
-    dfree(d_leaves, st);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     KD_CUDA(cudaStreamSynchronize(st));
