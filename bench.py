@@ -369,9 +369,10 @@ def run_b200(args):
             ctr_src = f"SURVEY §8(d) reference counters for {args.config}"
         qb = query_bytes(w.dims, w.k, v_ref, c_ref)
         ach_q = q * qb / tq / 1e9
-        # build: 10 launches per level + k_subtree, 2 per level preorder stitch, relocate, ids, leaf count;
-        # query: home-leaf keys, 5 CUB radix-sort kernels, k_knn_persist
-        launches = 12 * levels + 4 + 7
+        # build: 10 per breadth-first level (sample, tile info, hist, select, slow, tile-left, 2 scan,
+        # scatter, children) + 2 per level preorder stitch + subtree, relocate, ids;
+        # query: 3-D Morton keys (box + keys), 6 CUB radix-sort kernels (32-bit keys), KNN (ncu list: 204 on C2)
+        launches = 12 * levels + 3 + (9 if w.dims == 3 else 7)
         traffic = measured_traffic(args.config)
         line = {
             "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
