@@ -227,6 +227,39 @@ def test_large_uniform_tree_and_sampled_knn(api, oracle):
     assert np.array_equal(d, bd) and np.array_equal(i, bi)
 
 
+def test_big_root_node_tree_parity(api, oracle):
+    """A 5M-point clustered set: the root level exceeds 2^22 points (64-bit Fisher-Yates
+    keys in k_sample) -- whole tree byte-equal to the oracle."""
+    core, lt, lq = api
+    rows = make_rows(5_000_000, 3, 91, "halo-f32")
+    ps = core.PointSet.from_rows(rows)
+    tree = lt.build_local_tree(ps, lt.BuildConfig(seed=13))
+    ref = oracle.build_tree(ps.coords, ps.ids, seed=13)
+    for key in ("node_dim", "node_value", "node_left", "node_right", "node_count"):
+        assert np.array_equal(getattr(tree, key), getattr(ref, key)), key
+    assert np.array_equal(tree.points.ids, ref.ids) and tree.depth == ref.depth
+
+
+def test_large_duplicate_heavy_tree_parity(api, oracle):
+    """1.5M points, 40 % of them stacked on 50 sites: degenerate breadth-first nodes,
+    constant dimensions, exact-fallback splits -- tree byte-equal, KNN equal to brute force."""
+    core, lt, lq = api
+    rng = np.random.default_rng(92)
+    base = rng.random((900_000, 3), dtype=np.float32)
+    sites = rng.random((50, 3), dtype=np.float32)
+    rows = np.concatenate([base, sites[rng.integers(0, 50, 600_000)]]).astype(np.float64)
+    ps = core.PointSet.from_rows(rows)
+    tree = lt.build_local_tree(ps, lt.BuildConfig(seed=14))
+    ref = oracle.build_tree(ps.coords, ps.ids, seed=14)
+    for key in ("node_dim", "node_value", "node_left", "node_right", "node_count"):
+        assert np.array_equal(getattr(tree, key), getattr(ref, key)), key
+    assert np.array_equal(tree.points.ids, ref.ids)
+    q = np.concatenate([sites[:20], rng.random((980, 3), dtype=np.float32)]).astype(np.float64)
+    d, i, c, _ = lq.find_knn_batch(tree, q, 8)
+    bd, bi, bc = oracle.brute_knn(ps.coords, ps.ids, q, 8)
+    assert np.array_equal(c, bc) and np.array_equal(d, bd) and np.array_equal(i, bi)
+
+
 class TestReferenceSemantics:
     """Reference test cases re-pointed at the drop-in (pkg/tests/test_local_query.py, test_local_tree.py)."""
 
