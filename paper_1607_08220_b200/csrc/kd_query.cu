@@ -598,11 +598,13 @@ constexpr int WQ_DC = 16;  // max dimensions
 template <typename T, int KM, int DCAP>
 __global__ void __launch_bounds__(WQ_WARPS * 32)
 k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
-         const uint64_t* __restrict__ ids, int64_t n, int D, const double* __restrict__ queries,
+         const uint64_t* __restrict__ ids, int64_t n, int D_rt, const double* __restrict__ queries,
          const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
          const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
          int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter) {
     constexpr int DC = DCAP;  // register arrays sized for the dimension count (10 for C4, else 16)
+    // an instance for one exact dimension count folds every `d < D` test at compile time
+    const int D = DCAP != WQ_DC ? DCAP : D_rt;
     __shared__ int s_node[WQ_WARPS][QCAP];
     __shared__ float s_off[WQ_WARPS][QCAP][32];
     __shared__ double s_q[WQ_WARPS][DC];
@@ -693,8 +695,15 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                 for (int h = 0; h < 2; h++) {
                     const int j = c + h * 32 + lane;
 #pragma unroll
-                    for (int d = 0; d < DC; d++)
-                        if (d < D) cv[h][d] = j < len ? coords[(int64_t)d * n + start + j] : T(0);
+                    for (int d = 0; d < DC; d++) cv[h][d] = T(0);
+                    if (j < len) {  // one guard per point; the dimension rows by pointer steps
+                        const T* pp = coords + start + j;
+#pragma unroll
+                        for (int d = 0; d < DC; d++) {
+                            if (d < D) cv[h][d] = *pp;
+                            pp += n;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
@@ -860,7 +869,7 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
                                                      a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
                 cudaFreeAsync(ctr, st);
             };
-            if (t.dims <= 10) go(k_knn_wq<T, KM, 10>);
+            if (t.dims == 10) go(k_knn_wq<T, KM, 10>);  // exact-dimension instance (C4)
             else go(k_knn_wq<T, KM, WQ_DC>);
             return;
         }
