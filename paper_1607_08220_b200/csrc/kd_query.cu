@@ -650,10 +650,9 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                              ((1.0 - 2.0 * u) * (1.0 - 2.0 * u)) * (1.0 + 1e-12);
             return t >= 3.0e38 ? INFINITY : __double2float_ru(t);
         };
-        double bd[KM];
-        uint32_t bp[KM];
-#pragma unroll
-        for (int j = 0; j < KM; j++) { bd[j] = INFINITY; bp[j] = 0; }
+        // the sorted list is lane-distributed: lane j holds entry j (k + 1 <= 32)
+        double my_d = INFINITY;
+        uint32_t my_p = 0;
         int cnt = 0;
         double kth_d = radius;
         uint32_t kth_p = 0;
@@ -741,9 +740,17 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                         const double dd = __shfl_sync(FULL, dist, src);
                         const uint32_t pos = (uint32_t)(start + cc + src);
                         if (cnt < kk ? dd < radius : (dd <= kth_d && lexless_pos(dd, pos, kth_d, kth_p, ids))) {
-                            topk_insert_pos<KM>(bd, bp, cnt, kk, dd, pos, ids);
+                            // entries preceding (dd, pos) form a prefix of the lanes; ids only on ties
+                            const bool before = lane < cnt && (my_d < dd || (my_d == dd && ids[my_p] < ids[pos]));
+                            const int at = __popc(__ballot_sync(FULL, before));
+                            const double up_d = __shfl_up_sync(FULL, my_d, 1);
+                            const uint32_t up_p = __shfl_up_sync(FULL, my_p, 1);
+                            if (lane > at && lane < kk) { my_d = up_d; my_p = up_p; }
+                            if (lane == at) { my_d = dd; my_p = pos; }
+                            if (cnt < kk) cnt++;
                             if (cnt == kk) {
-                                topk_last<KM>(bd, bp, kk, kth_d, kth_p);
+                                kth_d = __shfl_sync(FULL, my_d, kk - 1);
+                                kth_p = __shfl_sync(FULL, my_p, kk - 1);
                                 if constexpr (sizeof(T) == 4) thr32 = make_thr(kth_d);
                             }
                         }
@@ -763,22 +770,16 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                 c0++;
             }
         }
-        // results (lane w writes row entry w)
-        int w = 0;
-        bool dropped = false;
-#pragma unroll
-        for (int j = 0; j < KM; j++) {
-            if (j < cnt) {
-                const uint64_t id = ids[bp[j]];
-                if (has_ex && !dropped && id == ex) {
-                    dropped = true;
-                } else if (w < k) {
-                    if (lane == w) {
-                        out_d[qi * (int64_t)k + w] = bd[j];
-                        out_i[qi * (int64_t)k + w] = id;
-                    }
-                    w++;
-                }
+        // results: lane j holds entry j; the excluded id (if present) is dropped
+        const uint64_t my_id = lane < cnt ? ids[my_p] : 0;
+        const unsigned exm = __ballot_sync(FULL, has_ex && lane < cnt && my_id == ex);
+        const int drop = exm ? __ffs(exm) - 1 : 32;
+        const int w = min(cnt - (exm ? 1 : 0), k);
+        if (lane < cnt && lane != drop) {
+            const int slot = lane - (lane > drop ? 1 : 0);
+            if (slot < k) {
+                out_d[qi * (int64_t)k + slot] = my_d;
+                out_i[qi * (int64_t)k + slot] = my_id;
             }
         }
         if (lane == 0) {
