@@ -596,7 +596,7 @@ constexpr int WQ_WARPS = 4;
 constexpr int WQ_DC = 16;  // max dimensions
 
 template <typename T, int KM, int DCAP>
-__global__ void __launch_bounds__(WQ_WARPS * 32)
+__global__ void __launch_bounds__(WQ_WARPS * 32, DCAP == WQ_DC ? 5 : 6)
 k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
          const uint64_t* __restrict__ ids, int64_t n, int D_rt, const double* __restrict__ queries,
          const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
