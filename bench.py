@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """Benchmark: kd-tree build (Mpoints/s) + exact KNN (queries/s) on B200.
 
-Workload (BASELINE.json configs[1], SURVEY §8(d) "C2"): 64,000,000 clustered 3D
-float32 points (4096 Gaussian halos + 20 % uniform background, periodic box),
-16,000,000 queries drawn from the dataset rows with the self-match excluded,
-k=5, leaf bucket 32.  One step = build the whole kd-tree + answer every query.
+Workload (BASELINE.json configs[2], SURVEY §8(d) "C3" -- the metric's "k=5 at
+1/2/4/8 B200" config and the largest that fits one GPU): 256,000,000 float32
+3D points in [0,1]x[0,0.5]x[0,0.25] (x, z uniform; y from a Harris current
+sheet sech^2((y-0.25)/0.01) plus a 10 % uniform floor), 64,000,000 queries of
+the same law, k=5, leaf bucket 32.  One step = build the whole kd-tree +
+answer every query.  ``--config C1|C2|C4`` selects the other configs.
 
 Printed JSON (one line, rank 0):
   value        build throughput, device-resident inputs (Mpoints/s)
@@ -44,7 +46,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4"])
     p.add_argument("--points", dest="n", type=int, default=None, help="override points per GPU (debug)")
     p.add_argument("--queries", dest="q", type=int, default=None, help="override queries per GPU (debug)")
     p.add_argument("--no-e2e", action="store_true")
@@ -52,6 +54,9 @@ def parse():
     p.add_argument("--cpu-build-sample", type=int, default=4_000_000)
     p.add_argument("--cpu-query-sample", type=int, default=200_000)
     return p.parse_args()
+
+
+METRIC = "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline"
 
 
 def peaks():
@@ -122,12 +127,16 @@ def build_bytes(n, dims, leaf):
 def measured_traffic(config):
     """ncu DRAM bytes (read + write) per build and per query batch, committed under
     profiles/ by tools/traffic.py (C2 only; {} when absent)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"r01_traffic_{config.lower()}.json")
-    try:
-        with open(path) as f:
-            return json.load(f)
-    except (OSError, ValueError):
-        return {}
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_traffic_{config.lower()}.json")
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            d["file"] = os.path.relpath(path, ROOT)
+            return d
+        except (OSError, ValueError):
+            continue
+    return {}
 
 
 def query_bytes(dims, k, v, c):
@@ -158,14 +167,42 @@ def cpu_baseline_leg(cfgname, w, tree, sel_queries, args, seed=0):
     qs = sel_queries
     kk = w.k + (1 if w.queries_from_data else 0)
     t0 = time.perf_counter()
-    _, _, _, ctr = O.knn(otree, qs, kk, threads=cores)
+    rd, ri, rc, ctr = O.knn(otree, qs, kk, threads=cores)
     tq = time.perf_counter() - t0
     return {
+        "rows": (rd, ri, rc),
         "build_mpts_s": nb / tb / 1e6, "build_sample_points": nb, "build_s": tb,
         "knn_q_s": qs.shape[0] / tq, "knn_sample_queries": int(qs.shape[0]), "knn_s": tq,
         "ref_nodes_visited": float(ctr[:, 0].mean()), "ref_points_compared": float(ctr[:, 2].mean()),
         "cores": cores,
     }
+
+
+def reference_rows_check(ref_rows, od, oi, oc, excl, k):
+    """This step's GPU rows for the first nq queries vs the reference traversal
+    (oracle port of local_query.py:72-172) over the identical full-size tree.
+    With self-exclusion the reference side is its k+1 search minus the query's
+    own id, truncated to k.  Rows may differ only where the reference's
+    bound >= r' pruning drops an exact tie: counted, not hidden."""
+    import numpy as np
+    rd, ri, rc = ref_rows
+    nq = rd.shape[0]
+    gd, gi, gc = od.cpu().numpy(), oi.cpu().numpy().view(np.uint64), oc.cpu().numpy()
+    if excl is not None:
+        ex = excl.cpu().numpy().astype(np.uint64)
+        keep = (ri != ex[:, None]) & (np.arange(ri.shape[1])[None, :] < rc[:, None])
+        pos = np.cumsum(keep, 1) - 1
+        wd = np.zeros((nq, k)); wi = np.zeros((nq, k), np.uint64)
+        sel = keep & (pos < k)
+        r_idx, c_idx = np.nonzero(sel)
+        wd[r_idx, pos[sel]] = rd[sel]
+        wi[r_idx, pos[sel]] = ri[sel]
+        rd, ri, rc = wd, wi, np.minimum(keep.sum(1), k)
+    m = np.arange(k)[None, :] < gc[:, None]
+    same = (gc == rc) & np.all(np.where(m, gd == rd[:, :k], True), 1) & np.all(np.where(m, gi == ri[:, :k], True), 1)
+    return {"queries": int(nq), "rows_equal": int(same.sum()), "equal": bool(same.all()),
+            "vs": "reference traversal (C oracle port) over the identical full-size tree: ids identical, "
+                  "f64 distances bit-identical"}
 
 
 def run_reference(args):
@@ -203,11 +240,15 @@ def run_reference(args):
     tb, tq = float(np.mean(tb_all)), float(np.mean(tq_all))
     value = nb / tb / 1e6
     line = {
-        "impl": "reference", "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "Mpoints/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "n": w.n, "q": w.q, "k": w.k, "leaf": w.leaf, "dims": w.dims},
+        "config": {"workload": w.name, "n": nb, "q": len(sel), "k": w.k, "leaf": w.leaf, "dims": w.dims,
+                   "workload_n": w.n, "workload_q": w.q,
+                   "sample": f"each step builds a {nb}-point tree of the {w.name} law and answers {len(sel)} "
+                             f"queries against it (rates; the full {w.n}-point build takes minutes per step "
+                             f"on the host)"},
         "knn": {"value": len(sel) / tq, "unit": "queries/s"},
         "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": cores, "kind": "port",
                          "sample": f"build of {nb} points of the {w.name} law + {len(sel)} self-excluded "
@@ -350,10 +391,13 @@ def run_b200(args):
         del h_coords, h_q, h_ex, h_d, h_i, h_c
 
     cpu = None
+    ref_check = None
     if rank == 0 and not args.no_cpu_baseline:
         nqs = min(args.cpu_query_sample if w.dims <= 3 else 2000, q)  # 10-D queries scan ~1e5 points each
         qsel = queries[:nqs].cpu().numpy()
         cpu = cpu_baseline_leg(args.config, w, tree, qsel, args)
+        ref_check = reference_rows_check(cpu.pop("rows"), od[:nqs], oi[:nqs], oc[:nqs],
+                                         None if excl is None else excl[:nqs], w.k)
 
     if rank == 0:
         peak, peak_kind = peaks()
@@ -375,7 +419,7 @@ def run_b200(args):
         launches = 12 * levels + 3 + (9 if w.dims == 3 else 7)
         traffic = measured_traffic(args.config)
         line = {
-            "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
+            "metric": METRIC,
             "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -396,7 +440,8 @@ def run_b200(args):
                                  "kernel": "query batch (home-leaf sort + k_knn_persist)",
                                  "bytes_per_query": qb, "model": "4D+8V+4DC+16k", "V": v_ref, "C": c_ref,
                                  "counters": ctr_src}},
-            "sample_check_vs_fp64_bruteforce": ok,
+            "sample_check_vs_fp64_bruteforce": {"queries": min(16, q), "equal": ok},
+            "sample_check_vs_reference_traversal": ref_check,
             "build_levels": levels,
             "build_slow_nodes": slow_nodes,
             "gpu_launches": launches,
@@ -516,7 +561,7 @@ def run_b200_multi(args):
         bbytes, levels_model = build_bytes(n, w.dims, w.leaf)
         ach_b = bbytes / tb / 1e9
         line = {
-            "metric": "kd-tree build Mpoints/s and KNN queries/s (k=5) at 1/2/4/8 B200 vs HBM roofline",
+            "metric": METRIC,
             "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
