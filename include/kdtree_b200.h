@@ -57,6 +57,7 @@ extern "C" {
 #define KD_DEVICE_PTRS 1u     /* all array arguments are device pointers */
 #define KD_NO_SORT 2u         /* kd_knn: keep caller query order (no leaf sort) */
 #define KD_THREAD_PER_QUERY 4u /* kd_knn: one thread per query, no dynamic fetch (default: persistent warps) */
+#define KD_KNN_PACKET 8u      /* kd_knn, D <= 3: one warp per 32-query packet over tight boxes (default: per-lane traversals) */
 
 typedef struct kd_tree kd_tree;
 
@@ -82,6 +83,9 @@ typedef struct {
     int64_t build_levels;     /* breadth-first global-memory levels */
     int64_t build_tasks;      /* shared-memory subtree tasks */
     int64_t build_slow_nodes; /* nodes resolved by the exact slow path */
+    double build_ms_levels;   /* breadth-first levels (sampling, histograms, partitions) */
+    double build_ms_subtree;  /* shared-memory subtree kernel */
+    double build_ms_finish;   /* preorder stitch, relocation, id gather */
 } kd_tree_info;
 
 /* Reference LocalTree layout (local_tree.py:71-108).  Export fills caller

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("KDB_LIB_PATH") or os.path.join(_HERE, "libkdtree_b200
 
 KD_OK, KD_EINVAL, KD_ECUDA, KD_EUNSUPPORTED, KD_ENOMEM = 0, -1, -2, -3, -4
 KD_F32, KD_F64 = 1, 2
-KD_DEVICE_PTRS, KD_NO_SORT, KD_THREAD_PER_QUERY = 1, 2, 4
+KD_DEVICE_PTRS, KD_NO_SORT, KD_THREAD_PER_QUERY, KD_KNN_PACKET = 1, 2, 4, 8
 
 EXPORTED = ("kd_version", "kd_last_error", "kd_device_count", "kd_tree_build", "kd_tree_import",
             "kd_tree_get_info", "kd_tree_export", "kd_knn", "kd_tree_free", "kd_histogram", "kd_partition",
@@ -32,7 +32,8 @@ class kd_tree_info(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("n", C.c_int64), ("n_leaves", C.c_int64), ("depth", C.c_int64),
                 ("dims", C.c_int32), ("dtype", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32),
                 ("build_ms", C.c_double), ("build_levels", C.c_int64), ("build_tasks", C.c_int64),
-                ("build_slow_nodes", C.c_int64)]
+                ("build_slow_nodes", C.c_int64), ("build_ms_levels", C.c_double),
+                ("build_ms_subtree", C.c_double), ("build_ms_finish", C.c_double)]
 
 
 class kd_tree_arrays(C.Structure):

@@ -1733,14 +1733,81 @@ static __global__ void k_gather_ids(const uint64_t* __restrict__ ids_in, const i
 // ============================================================================
 // host orchestration
 // ============================================================================
+static bool trace_alloc() {
+    static const bool v = std::getenv("KDB_TRACE_ALLOC") != nullptr;
+    return v;
+}
+
+// Build scratch comes from a per-device arena of persistent chunks reused by every
+// build (bump allocation, reset per build): the stream-ordered pool stalled for
+// 10-400 ms on some of a 256M-point build's ~100 allocations (growth/remapping of a
+// fragmented pool), while a build's allocation sequence is the same from one build to
+// the next, so the chunks fit again without touching the driver.  Only the buffers
+// the tree keeps (packed coordinates, row ids, ids, nodes, counts) use the pool.
+struct Arena {
+    int device = 0;
+    struct Chunk {
+        char* base;
+        size_t size;
+    };
+    std::vector<Chunk> chunks;
+    size_t ci = 0, off = 0;
+    void reset() { ci = 0; off = 0; }
+    bool owns(const void* p) const {
+        for (const Chunk& c : chunks)
+            if ((const char*)p >= c.base && (const char*)p < c.base + c.size) return true;
+        return false;
+    }
+    void* alloc(size_t bytes) {
+        bytes = (std::max<size_t>(bytes, 1) + 255) & ~(size_t)255;
+        while (ci < chunks.size()) {
+            if (off + bytes <= chunks[ci].size) {
+                void* p = chunks[ci].base + off;
+                off += bytes;
+                return p;
+            }
+            ci++;
+            off = 0;
+        }
+        const size_t sz = std::max<size_t>(bytes, (size_t)1 << 28);
+        char* p = nullptr;
+        KD_CUDA(cudaMalloc(&p, sz));  // growth only (first build of a size)
+        chunks.push_back({p, sz});
+        off = bytes;
+        return p;
+    }
+};
+Arena* arena_acquire(int device);  // kd_build_f32.cu (one free list per device)
+void arena_release(Arena* a);
+static thread_local Arena* t_arena = nullptr;
+
+struct ArenaScope {  // the calling thread's builds allocate scratch from `a` while in scope
+    Arena* a;
+    explicit ArenaScope(int device) : a(arena_acquire(device)) { t_arena = a; }
+    ~ArenaScope() {
+        t_arena = nullptr;
+        arena_release(a);
+    }
+};
+
 template <typename X>
-static X* dalloc(size_t count, cudaStream_t st) {
+static X* palloc(size_t count, cudaStream_t st) {  // pool: buffers that outlive the build
     void* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     KD_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(X), st));
+    if (trace_alloc()) {
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 0.5) fprintf(stderr, "[kdb] slow cudaMallocAsync %.3f ms for %zu bytes\n", ms, count * sizeof(X));
+    }
     return static_cast<X*>(p);
 }
+template <typename X>
+static X* dalloc(size_t count, cudaStream_t st) {  // build scratch
+    if (t_arena) return static_cast<X*>(t_arena->alloc(std::max<size_t>(count, 1) * sizeof(X)));
+    return palloc<X>(count, st);
+}
 static void dfree(void* p, cudaStream_t st) {
-    if (p) cudaFreeAsync(p, st);
+    if (p && !(t_arena && t_arena->owns(p))) cudaFreeAsync(p, st);
 }
 
 // keep freed stream-ordered allocations in the pool across the per-level host
@@ -1770,6 +1837,26 @@ uint32_t* fy_slots(int device, cudaStream_t st) {
     return slots[device];
 }
 
+static std::vector<Arena*> g_arenas[64];
+Arena* arena_acquire(int device) {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    std::vector<Arena*>& fl = g_arenas[device & 63];
+    Arena* a = nullptr;
+    if (!fl.empty()) {
+        a = fl.back();
+        fl.pop_back();
+    } else {
+        a = new Arena();
+        a->device = device;
+    }
+    a->reset();
+    return a;
+}
+void arena_release(Arena* a) {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    g_arenas[a->device & 63].push_back(a);
+}
+
 void retain_pool(int device) {
     static bool done[64] = {false};
     std::lock_guard<std::mutex> lk(g_init_mu);
@@ -1792,6 +1879,11 @@ struct HostTrace {
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         fprintf(stderr, "[kdb] %9.3f ms  %s %d\n", ms, what, a);
     }
+    void sync_mark(cudaStream_t st, const char* what, int a = -1) {  // tracing only: waits for the stream
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        mark(what, a);
+    }
 };
 
 template <typename T>
@@ -1799,9 +1891,11 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
                 KdTreeDev* out, BuildStats* stats) {
     HostTrace tr;
     tr.mark("enter");
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, e_top, e_sub;
     KD_CUDA(cudaEventCreate(&e0));
     KD_CUDA(cudaEventCreate(&e1));
+    KD_CUDA(cudaEventCreate(&e_top));
+    KD_CUDA(cudaEventCreate(&e_sub));
     KD_CUDA(cudaEventRecord(e0, st));
     out->dims = dims;
     out->n = n;
@@ -1810,12 +1904,13 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     retain_pool(out->device);
     if (n == 0) {
         out->n_nodes = 0; out->n_leaves = 0; out->depth = 0;
-        out->nodes = dalloc<KdNode>(1, st);
-        out->node_count = dalloc<int32_t>(1, st);
-        out->coords = dalloc<T>(1, st);
-        out->ids = dalloc<uint64_t>(1, st);
-        out->perm = dalloc<int32_t>(1, st);
+        out->nodes = palloc<KdNode>(1, st);
+        out->node_count = palloc<int32_t>(1, st);
+        out->coords = palloc<T>(1, st);
+        out->ids = palloc<uint64_t>(1, st);
+        out->perm = palloc<int32_t>(1, st);
         KD_CUDA(cudaStreamSynchronize(st));
+        cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e_top); cudaEventDestroy(e_sub);
         return;
     }
     DevCtx c;
@@ -1832,8 +1927,10 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     while (c.ts > 32 && sub_smem_bytes(c.ts, dims, sizeof(T)) > (size_t)dev_smem) c.ts /= 2;
     c.ts = std::max<int>(c.ts, 1);
 
-    T* buf[2] = {dalloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
-    int32_t* idx[2] = {dalloc<int32_t>(n, st), dalloc<int32_t>(n, st)};
+    ArenaScope arena(out->device);
+    // buf[0] / idx[0] end as the tree's packed coordinates / row ids
+    T* buf[2] = {palloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
+    int32_t* idx[2] = {palloc<int32_t>(n, st), dalloc<int32_t>(n, st)};
 
     // top store (grown per level)
     size_t ts_cap = 1024;
@@ -2032,6 +2129,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     tr.mark("top phase done");
     const int ntasks = ntasks_known > 0 ? ntasks_known : 1;
     // subtree phase
+    KD_CUDA(cudaEventRecord(e_top, st));
+    tr.sync_mark(st, "top scratch freed");
     KdNode* scratch = dalloc<KdNode>(2 * (size_t)n + 2, st);
     int32_t* scnt = dalloc<int32_t>(2 * (size_t)n + 2, st);
     int32_t* task_nodes = dalloc<int32_t>(ntasks, st);
@@ -2040,6 +2139,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     const size_t sub_smem = sub_smem_bytes(c.ts, dims, sizeof(T));
     SubStack* sstack = dalloc<SubStack>(2 * (size_t)n + 2, st);
     uint32_t* fyslots = fy_slots(out->device, st);
+    tr.sync_mark(st, "subtree scratch allocated");
     int* fylocks = reinterpret_cast<int*>(fyslots + (size_t)FY_SLOTS * 2 * MAXS);
     if (dims == 3) {
         KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
@@ -2051,6 +2151,8 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
                                                       fyslots, fylocks, task_nodes, task_depth);
     }
     KD_CUDA(cudaGetLastError());
+    KD_CUDA(cudaEventRecord(e_sub, st));
+    tr.sync_mark(st, "k_subtree done", ntasks);
     // top counts bottom-up, preorder top-down
     for (int L = (int)levels.size() - 1; L >= 0; L--)
         k_top_count<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes);
@@ -2064,13 +2166,15 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         if (root_kind == TS_TASK) KD_CUDA(cudaMemsetAsync(task_base, 0, sizeof(int32_t), st));
         KD_CUDA(cudaStreamSynchronize(st));
     }
-    KdNode* nodes = dalloc<KdNode>(total_nodes, st);
-    int32_t* ncount = dalloc<int32_t>(total_nodes, st);
+    KdNode* nodes = palloc<KdNode>(total_nodes, st);
+    int32_t* ncount = palloc<int32_t>(total_nodes, st);
     for (size_t L = 0; L < levels.size(); L++)
         k_top_pre<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes, task_base, nodes,
                                                             ncount);
+    tr.sync_mark(st, "preorder done");
     k_relocate<<<ntasks, 256, 0, st>>>(tasks, task_nodes, task_base, scratch, scnt, nodes, ncount);
-    uint64_t* ids_out = dalloc<uint64_t>(n, st);
+    tr.sync_mark(st, "relocate done");
+    uint64_t* ids_out = palloc<uint64_t>(n, st);
     k_gather_ids<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_ids, idx[0], ids_out, n);
     KD_CUDA(cudaGetLastError());
     // depth = max(task depths, top levels)
@@ -2093,6 +2197,13 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         stats->ms_total = ms;
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, e0, e_top);
+        cudaEventElapsedTime(&b, e_top, e_sub);
+        cudaEventElapsedTime(&c, e_sub, e1);
+        stats->ms_levels = a;
+        stats->ms_subtree = b;
+        stats->ms_finish = c;
         stats->levels = (int)levels.size();
         stats->tasks = ntasks_known;
         stats->slow_nodes = slow_total;
@@ -2105,14 +2216,24 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     dfree(scratch, st); dfree(scnt, st); dfree(sstack, st); dfree(task_nodes, st); dfree(task_depth, st); dfree(task_base, st);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(e_top);
+    cudaEventDestroy(e_sub);
     KD_CUDA(cudaStreamSynchronize(st));
     tr.mark("exit");
 }
 
 #ifdef KD_BUILD_COMMON
+// every tree buffer comes from the device's stream-ordered pool (cudaMallocAsync); freeing
+// with cudaFreeAsync returns it to the pool.  (cudaFree would hand the physical pages
+// back to the driver, and the next build would pay for re-mapping them: measured
+// 10-200 ms stalls in the first breadth-first level of a 256M-point build.)
 void free_tree(KdTreeDev* t) {
     if (!t) return;
-    cudaFree(t->nodes); cudaFree(t->node_count); cudaFree(t->coords); cudaFree(t->ids); cudaFree(t->perm);
+    for (void* p : {(void*)t->nodes, (void*)t->node_count, t->coords, (void*)t->ids, (void*)t->perm,
+                    (void*)t->qnodes})
+        if (p) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+    t->qnodes = nullptr;
     t->nodes = nullptr; t->node_count = nullptr; t->coords = nullptr; t->ids = nullptr; t->perm = nullptr;
 }
 

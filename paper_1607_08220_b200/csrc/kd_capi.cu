@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,6 +19,7 @@ using namespace kdb;
 struct kd_tree {
     KdTreeDev dev;
     BuildStats stats;
+    std::mutex mu;  // guards the lazily built query tree
 };
 
 static thread_local std::string g_err;
@@ -190,11 +192,12 @@ int kd_tree_import(const kd_tree_arrays* a, int64_t n_nodes, int64_t n, int dims
         KdTreeDev& d = t->dev;
         d.device = device; d.dims = dims; d.dtype = dtype; d.n = n; d.n_nodes = n_nodes; d.depth = depth;
         const int64_t nn1 = n_nodes > 0 ? n_nodes : 1, n1 = n > 0 ? n : 1;
-        KD_CUDA(cudaMalloc(&d.nodes, nn1 * sizeof(KdNode)));
-        KD_CUDA(cudaMalloc(&d.node_count, nn1 * sizeof(int32_t)));
-        KD_CUDA(cudaMalloc(&d.ids, n1 * 8));
-        KD_CUDA(cudaMalloc(&d.perm, n1 * 4));
-        KD_CUDA(cudaMalloc(&d.coords, (size_t)dims * n1 * (dtype == KD_F32 ? 4 : 8)));
+        retain_pool(device);
+        KD_CUDA(cudaMallocAsync((void**)&d.nodes, nn1 * sizeof(KdNode), st));
+        KD_CUDA(cudaMallocAsync((void**)&d.node_count, nn1 * sizeof(int32_t), st));
+        KD_CUDA(cudaMallocAsync((void**)&d.ids, n1 * 8, st));
+        KD_CUDA(cudaMallocAsync((void**)&d.perm, n1 * 4, st));
+        KD_CUDA(cudaMallocAsync(&d.coords, (size_t)dims * n1 * (dtype == KD_F32 ? 4 : 8), st));
         if (n_nodes > 0) {
             DevBuf bdim(nn1 * 4, st), bval(nn1 * 8, st), bl(nn1 * 4, st), br(nn1 * 4, st), bc(nn1 * 8, st), bad(4, st);
             KD_CUDA(cudaMemcpyAsync(bdim.p, a->node_dim, n_nodes * 4, cudaMemcpyHostToDevice, st));
@@ -249,6 +252,9 @@ int kd_tree_get_info(const kd_tree* t, kd_tree_info* info) {
     info->dtype = t->dev.dtype;
     info->device = t->dev.device;
     info->build_ms = t->stats.ms_total;
+    info->build_ms_levels = t->stats.ms_levels;
+    info->build_ms_subtree = t->stats.ms_subtree;
+    info->build_ms_finish = t->stats.ms_finish;
     info->build_levels = t->stats.levels;
     info->build_tasks = t->stats.tasks;
     info->build_slow_nodes = t->stats.slow_nodes;
@@ -309,7 +315,11 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
     if (nq < 0) return fail(KD_EINVAL, "nq must be >= 0");
     if (nq >= (int64_t(1) << 31)) return fail(KD_EUNSUPPORTED, "nq must be < 2^31 per call");
     if (nq > 0 && (!queries || !out_d || !out_i || !out_c)) return fail(KD_EINVAL, "NULL query/output buffer");
-    if (t->dev.depth > KNN_MAX_DEPTH)
+    // the packet kernel (D <= 3, k(+1) <= 32) sizes its stack from the tree depth; the
+    // per-query kernels carry a fixed stack
+    const bool packet = (flags & KD_KNN_PACKET) && t->dev.dims <= 3 && k + (exclude_ids ? 1 : 0) <= 32 &&
+                        !(flags & KD_THREAD_PER_QUERY);
+    if (!packet && t->dev.depth > KNN_MAX_DEPTH)
         return fail(KD_EUNSUPPORTED, "tree deeper than the device traversal stack (" +
                                          std::to_string(KNN_MAX_DEPTH) + ")");
     if (nq == 0) return KD_OK;
@@ -324,6 +334,11 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.k = k;
         a.sort_queries = !(flags & KD_NO_SORT);
         a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
+        a.packet = (flags & KD_KNN_PACKET) != 0;
+        if (a.packet) {  // the packet kernel's query tree (tight boxes) is built on first use
+            std::lock_guard<std::mutex> lk(const_cast<kd_tree*>(t)->mu);
+            if (!d.qnodes) build_qtree(const_cast<KdTreeDev*>(&d), st);
+        }
         DevBuf bq, br, be, bd, bi, bc, bctr;
         DevBuf hd, hi;
         if (k > 32 || (k == 32 && exclude_ids && !a.thread_per_query)) {  // heap kernel scratch

@@ -22,6 +22,7 @@
 
 #include "kd_common.cuh"
 #include "kd_query.cuh"
+#include "kd_topk.cuh"
 #include "kd_tree.cuh"
 #include "kd_warp.cuh"
 
@@ -32,57 +33,6 @@ constexpr int QCAP = 40;  // traversal stack capacity (tree depth + 2)
 // (measured 34 vs 44 ms on C2); in higher dimensions the binary64 leaf scan dominates and it pays off
 template <int DT>
 constexpr bool kPersistF32Filter = (DT == 0);
-
-__device__ __forceinline__ bool lexless(double d0, uint64_t i0, double d1, uint64_t i1) {
-    return d0 < d1 || (d0 == d1 && i0 < i1);
-}
-
-// same list keyed by (sq_dist, packed row): ids are only read to break exact
-// distance ties (lexicographic (d, id) order is preserved exactly)
-__device__ __forceinline__ bool lexless_pos(double d0, uint32_t p0, double d1, uint32_t p1,
-                                            const uint64_t* __restrict__ ids) {
-    return d0 < d1 || (d0 == d1 && ids[p0] < ids[p1]);
-}
-
-// insert into the ascending (d, packed row) list of capacity k <= KM (the caller
-// has checked that it enters): one descending pass, each slot keeps, shifts from
-// its predecessor, or takes the new entry; ids are read only on exact ties
-template <int KM>
-__device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
-                                                uint32_t p, const uint64_t* __restrict__ ids) {
-    const int last = cnt < k ? cnt : k - 1;
-    bool placed = false;
-#pragma unroll
-    for (int jj = KM - 1; jj >= 0; jj--) {
-        if (jj <= last && !placed) {
-            const int pj = jj > 0 ? jj - 1 : 0;
-            const bool shift = jj > 0 && (d < bd[pj] || (d == bd[pj] && ids[p] < ids[bp[pj]]));
-            if (shift) {
-                bd[jj] = bd[pj];
-                bp[jj] = bp[pj];
-            } else {
-                bd[jj] = d;
-                bp[jj] = p;
-                placed = true;
-            }
-        }
-    }
-    if (cnt < k) cnt++;
-}
-
-// slot k-1 of the list (a register move when the list is exactly k long)
-template <int KM>
-__device__ __forceinline__ void topk_last(const double (&bd)[KM], const uint32_t (&bp)[KM], int k, double& kd,
-                                          uint32_t& kp) {
-    if (k == KM) {
-        kd = bd[KM - 1];
-        kp = bp[KM - 1];
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < KM; j++)
-        if (j == k - 1) { kd = bd[j]; kp = bp[j]; }
-}
 
 template <int DT>
 struct Dims {
@@ -1027,6 +977,13 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
         cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
         KD_CUDA(cudaMallocAsync(&tmp, tb, st));
         cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
+    }
+    if (a.packet && knn_packet(t, a, order, st)) {
+        if (order) {
+            cudaFreeAsync(k0, st); cudaFreeAsync(k1, st); cudaFreeAsync(v0, st); cudaFreeAsync(order, st);
+            cudaFreeAsync(tmp, st);
+        }
+        return;
     }
     // the persistent kernel may jump straight to the home leaf only with home-leaf keys
     const uint32_t* home = (order && !(t.dims == 3 && knn_morton_order())) ? k1 : nullptr;

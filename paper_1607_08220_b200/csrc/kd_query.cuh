@@ -21,6 +21,7 @@ struct KnnArgs {
     uint64_t* heap_i = nullptr;
     bool sort_queries = true;
     bool thread_per_query = false;  // one-thread-per-query traversal (k > 32 always uses it)
+    bool packet = false;            // D <= 3: warp-per-packet kernel (kd_packet.cu) instead of per-lane traversals
 };
 
 constexpr int KNN_MAX_DEPTH = 37;  // traversal stack capacity - 3
@@ -28,5 +29,6 @@ constexpr int64_t KNN_CHUNK_MIN = 1 << 20;  // host-buffer pipeline: queries per
 constexpr int64_t KNN_MAX_CHUNKS = 8;
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st);
+bool knn_packet(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st);  // kd_packet.cu
 
 }  // namespace kdb

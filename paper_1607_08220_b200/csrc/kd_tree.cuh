@@ -17,6 +17,15 @@ struct __align__(16) KdNode {
     int32_t db;
 };
 
+// query-tree record for D <= 3 (kd_packet.cu): one per interior node, holding
+// both children's tight f32 bounding boxes (lo[0..2], hi[0..2]) and references
+// -- an interior child node index (count < 0) or a leaf bucket [ref, ref + count)
+struct __align__(16) QNode {
+    float lb[6];
+    float rb[6];
+    int32_t l, lc, r, rc;
+};
+
 enum { DT_F32 = 1, DT_F64 = 2 };
 
 struct KdTreeDev {
@@ -32,6 +41,7 @@ struct KdTreeDev {
     void* coords = nullptr;      // [dims][n] packed, float or double
     uint64_t* ids = nullptr;     // [n] packed ids
     int32_t* perm = nullptr;     // [n] packed row i holds input row perm[i]
+    QNode* qnodes = nullptr;     // [n_nodes] query tree (D <= 3; built with the tree)
 };
 
 struct BuildCfg {
@@ -43,6 +53,7 @@ struct BuildCfg {
 
 struct BuildStats {
     double ms_total = 0;
+    double ms_levels = 0, ms_subtree = 0, ms_finish = 0;  // phase split of ms_total
     int levels = 0;        // breadth-first (global-memory) levels
     int64_t tasks = 0;     // shared-memory subtree tasks
     int64_t slow_nodes = 0;  // nodes that needed the exact slow path
@@ -53,6 +64,7 @@ void build_tree(const T* d_coords_soa, const uint64_t* d_ids, int64_t n, int dim
                 cudaStream_t st, KdTreeDev* out, BuildStats* stats);
 
 void free_tree(KdTreeDev* t);
+void build_qtree(KdTreeDev* t, cudaStream_t st);  // kd_packet.cu
 void retain_pool(int device);
 
 }  // namespace kdb

@@ -127,7 +127,8 @@ class LocalTree:
         if self._native is None:
             return None
         inf = self._info
-        return {"build_ms": inf.build_ms, "levels": int(inf.build_levels), "tasks": int(inf.build_tasks),
+        return {"build_ms": inf.build_ms, "ms_levels": inf.build_ms_levels, "ms_subtree": inf.build_ms_subtree,
+                "ms_finish": inf.build_ms_finish, "levels": int(inf.build_levels), "tasks": int(inf.build_tasks),
                 "slow_nodes": int(inf.build_slow_nodes), "dtype": "f32" if inf.dtype == N.KD_F32 else "f64"}
 
     # -- device handle ---------------------------------------------------
