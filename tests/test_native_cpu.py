@@ -42,7 +42,7 @@ def test_library_is_sm100a():
 def test_struct_layouts_match_header():
     from paper_1607_08220_b200 import _native as N
     assert C.sizeof(N.kd_build_cfg) == 32
-    assert C.sizeof(N.kd_tree_info) == 4 * 8 + 4 * 4 + 8 + 3 * 8
+    assert C.sizeof(N.kd_tree_info) == 4 * 8 + 4 * 4 + 8 + 3 * 8 + 3 * 8
     assert C.sizeof(N.kd_tree_arrays) == 8 * 8
 
 
