@@ -32,6 +32,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "kd_arena.cuh"
 #include "kd_common.cuh"
 #include "kd_tree.cuh"
 #include "kd_warp.cuh"
@@ -1738,58 +1739,6 @@ static bool trace_alloc() {
     return v;
 }
 
-// Build scratch comes from a per-device arena of persistent chunks reused by every
-// build (bump allocation, reset per build): the stream-ordered pool stalled for
-// 10-400 ms on some of a 256M-point build's ~100 allocations (growth/remapping of a
-// fragmented pool), while a build's allocation sequence is the same from one build to
-// the next, so the chunks fit again without touching the driver.  Only the buffers
-// the tree keeps (packed coordinates, row ids, ids, nodes, counts) use the pool.
-struct Arena {
-    int device = 0;
-    struct Chunk {
-        char* base;
-        size_t size;
-    };
-    std::vector<Chunk> chunks;
-    size_t ci = 0, off = 0;
-    void reset() { ci = 0; off = 0; }
-    bool owns(const void* p) const {
-        for (const Chunk& c : chunks)
-            if ((const char*)p >= c.base && (const char*)p < c.base + c.size) return true;
-        return false;
-    }
-    void* alloc(size_t bytes) {
-        bytes = (std::max<size_t>(bytes, 1) + 255) & ~(size_t)255;
-        while (ci < chunks.size()) {
-            if (off + bytes <= chunks[ci].size) {
-                void* p = chunks[ci].base + off;
-                off += bytes;
-                return p;
-            }
-            ci++;
-            off = 0;
-        }
-        const size_t sz = std::max<size_t>(bytes, (size_t)1 << 28);
-        char* p = nullptr;
-        KD_CUDA(cudaMalloc(&p, sz));  // growth only (first build of a size)
-        chunks.push_back({p, sz});
-        off = bytes;
-        return p;
-    }
-};
-Arena* arena_acquire(int device);  // kd_build_f32.cu (one free list per device)
-void arena_release(Arena* a);
-static thread_local Arena* t_arena = nullptr;
-
-struct ArenaScope {  // the calling thread's builds allocate scratch from `a` while in scope
-    Arena* a;
-    explicit ArenaScope(int device) : a(arena_acquire(device)) { t_arena = a; }
-    ~ArenaScope() {
-        t_arena = nullptr;
-        arena_release(a);
-    }
-};
-
 template <typename X>
 static X* palloc(size_t count, cudaStream_t st) {  // pool: buffers that outlive the build
     void* p = nullptr;
@@ -1838,8 +1787,9 @@ uint32_t* fy_slots(int device, cudaStream_t st) {
 }
 
 static std::vector<Arena*> g_arenas[64];
+static std::mutex g_arena_mu;  // never held across a CUDA call (released from stream host callbacks)
 Arena* arena_acquire(int device) {
-    std::lock_guard<std::mutex> lk(g_init_mu);
+    std::lock_guard<std::mutex> lk(g_arena_mu);
     std::vector<Arena*>& fl = g_arenas[device & 63];
     Arena* a = nullptr;
     if (!fl.empty()) {
@@ -1853,7 +1803,7 @@ Arena* arena_acquire(int device) {
     return a;
 }
 void arena_release(Arena* a) {
-    std::lock_guard<std::mutex> lk(g_init_mu);
+    std::lock_guard<std::mutex> lk(g_arena_mu);
     g_arenas[a->device & 63].push_back(a);
 }
 

@@ -5,12 +5,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/kdtree_b200.h"
 #include "kd_common.cuh"
+#include "kd_arena.cuh"
 #include "kd_query.cuh"
 #include "kd_tree.cuh"
 
@@ -44,13 +46,23 @@ int kd_set_error(int code, const char* msg) { return fail(code, msg); }
 
 namespace {
 
+// scratch for one call: from the calling thread's arena inside an ArenaScope (synchronous
+// host-buffer paths), else from the stream-ordered pool
 struct DevBuf {
     void* p = nullptr;
     cudaStream_t st = nullptr;
+    bool arena = false;
     DevBuf() = default;
-    DevBuf(size_t bytes, cudaStream_t s) : st(s) { KD_CUDA(cudaMallocAsync(&p, bytes ? bytes : 1, s)); }
+    DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+        if (t_arena) {
+            p = t_arena->alloc(bytes);
+            arena = true;
+        } else {
+            KD_CUDA(cudaMallocAsync(&p, bytes ? bytes : 1, s));
+        }
+    }
     ~DevBuf() {
-        if (p) cudaFreeAsync(p, st);
+        if (p && !arena) cudaFreeAsync(p, st);
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -151,6 +163,8 @@ int kd_tree_build(const void* coords, int dtype, int64_t n, int dims, const uint
         DevBuf hc, hi;
         const void* dc = coords;
         const uint64_t* di = ids;
+        std::unique_ptr<ArenaScope> scope;
+        if (!dev_ptrs && n > 0) scope.reset(new ArenaScope(device));  // staging lives until the build returns
         if (!dev_ptrs && n > 0) {
             hc.~DevBuf();
             new (&hc) DevBuf((size_t)dims * n * es, st);
@@ -353,6 +367,7 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
             knn(d, a, st);
             return KD_OK;
         }
+        ArenaScope scope(d.device);  // synchronous below: staging from the arena
         // host buffers: device staging for the whole batch, then a pipeline over
         // query chunks -- H2D of chunk c+1 and D2H of chunk c-1 (copy engines, one
         // per direction) overlap the search of chunk c on the caller's stream
@@ -369,10 +384,27 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         }();
         const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(max_chunks, nq / KNN_CHUNK_MIN));
         const int64_t csz = (nq + nch - 1) / nch;
-        cudaStream_t s_in = nullptr, s_out = nullptr;
-        KD_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-        KD_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-        std::vector<cudaEvent_t> evs(2 * nch + 2, nullptr);
+        // copy streams + events; on every exit path (incl. a throw mid-pipeline) the guard waits
+        // for both copy streams and the caller's stream before the staging buffers go away
+        struct Pipe {
+            cudaStream_t s_in = nullptr, s_out = nullptr, st = nullptr;
+            std::vector<cudaEvent_t> evs;
+            ~Pipe() {
+                if (s_in) cudaStreamSynchronize(s_in);
+                if (s_out) cudaStreamSynchronize(s_out);
+                if (st) cudaStreamSynchronize(st);
+                for (auto& e : evs)
+                    if (e) cudaEventDestroy(e);
+                if (s_in) cudaStreamDestroy(s_in);
+                if (s_out) cudaStreamDestroy(s_out);
+            }
+        } pipe;
+        pipe.st = st;
+        KD_CUDA(cudaStreamCreateWithFlags(&pipe.s_in, cudaStreamNonBlocking));
+        KD_CUDA(cudaStreamCreateWithFlags(&pipe.s_out, cudaStreamNonBlocking));
+        cudaStream_t s_in = pipe.s_in, s_out = pipe.s_out;
+        pipe.evs.assign(2 * nch + 2, nullptr);
+        std::vector<cudaEvent_t>& evs = pipe.evs;
         for (auto& e : evs) KD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         KD_CUDA(cudaEventRecord(evs[2 * nch], st));  // staging allocated
         KD_CUDA(cudaStreamWaitEvent(s_in, evs[2 * nch], 0));
@@ -409,9 +441,6 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         KD_CUDA(cudaStreamWaitEvent(st, evs[2 * nch + 1], 0));
         KD_CUDA(cudaStreamSynchronize(s_out));
         KD_CUDA(cudaStreamSynchronize(st));
-        for (auto& e : evs) cudaEventDestroy(e);
-        cudaStreamDestroy(s_in);
-        cudaStreamDestroy(s_out);
     });
     return KD_OK;
 }

@@ -19,7 +19,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
+#include "kd_arena.cuh"
 #include "kd_common.cuh"
 #include "kd_query.cuh"
 #include "kd_topk.cuh"
@@ -27,6 +30,17 @@
 #include "kd_warp.cuh"
 
 namespace kdb {
+
+template <typename X>
+static X* scratch(size_t count, cudaStream_t st) {
+    if (t_arena) return static_cast<X*>(t_arena->alloc(std::max<size_t>(count, 1) * sizeof(X)));
+    void* p = nullptr;
+    KD_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(X), st));
+    return static_cast<X*>(p);
+}
+static void scratch_free(void* p, cudaStream_t st) {
+    if (p && !(t_arena && t_arena->owns(p))) cudaFreeAsync(p, st);
+}
 
 constexpr int QCAP = 40;  // traversal stack capacity (tree depth + 2)
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
@@ -812,13 +826,12 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
                 const long long want = (a.nq + WQ_WARPS - 1) / WQ_WARPS;
                 const unsigned grid =
                     (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
-                unsigned long long* ctr = nullptr;
-                KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
+                unsigned long long* ctr = scratch<unsigned long long>(1, st);
                 KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
                 kern<<<grid, WQ_WARPS * 32, 0, st>>>(t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n,
                                                      t.dims, a.queries, order, a.nq, (int)a.k, a.radii, a.excl,
                                                      a.out_d, a.out_i, a.out_c, a.out_ctr, ctr);
-                cudaFreeAsync(ctr, st);
+                scratch_free(ctr, st);
             };
             if (t.dims == 10) go(k_knn_wq<T, KM, 10>);  // exact-dimension instance (C4)
             else go(k_knn_wq<T, KM, WQ_DC>);
@@ -833,13 +846,12 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_persist<T, DT, KM>, threads, 0);
             const long long want = (a.nq + threads - 1) / threads;
             const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
-            unsigned long long* ctr = nullptr;
-            KD_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), st));
+            unsigned long long* ctr = scratch<unsigned long long>(1, st);
             KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
             k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
                 t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
                 (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, knn_push_free_first(), home);
-            cudaFreeAsync(ctr, st);
+            scratch_free(ctr, st);
             return;
         }
     }
@@ -947,25 +959,51 @@ static bool knn_morton_order() {
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
     if (a.nq == 0) return;
+    // temporaries (sort keys, CUB scratch, work counters) from an arena bound to the stream:
+    // the next call on the same stream reuses it in stream order (no allocation, no sync)
+    struct KnnArena {
+        std::unique_lock<std::mutex> lk;
+        Arena* prev;
+        KnnArena(int dev, cudaStream_t s) {
+            static std::mutex mu;
+            static std::map<std::pair<int, cudaStream_t>, std::pair<Arena*, std::mutex*>> by_stream;
+            std::pair<Arena*, std::mutex*> e;
+            {
+                std::lock_guard<std::mutex> g(mu);
+                auto it = by_stream.find({dev, s});
+                if (it == by_stream.end()) {
+                    Arena* a = new Arena();
+                    a->device = dev;
+                    it = by_stream.emplace(std::make_pair(dev, s), std::make_pair(a, new std::mutex())).first;
+                }
+                e = it->second;
+            }
+            lk = std::unique_lock<std::mutex>(*e.second);  // one host thread enqueues on a stream at a time
+            e.first->reset();
+            prev = t_arena;
+            t_arena = e.first;
+        }
+        ~KnnArena() { t_arena = prev; }
+    } ka(t.device, st);
     int32_t* order = nullptr;
     void* tmp = nullptr;
     uint32_t *k0 = nullptr, *k1 = nullptr;
     int32_t* v0 = nullptr;
     if (a.sort_queries && a.nq > 1 && t.n_nodes > 1) {
-        KD_CUDA(cudaMallocAsync((void**)&k0, a.nq * 4, st));
-        KD_CUDA(cudaMallocAsync((void**)&k1, a.nq * 4, st));
-        KD_CUDA(cudaMallocAsync((void**)&v0, a.nq * 4, st));
-        KD_CUDA(cudaMallocAsync((void**)&order, a.nq * 4, st));
+        k0 = scratch<uint32_t>(a.nq, st);
+        k1 = scratch<uint32_t>(a.nq, st);
+        v0 = scratch<int32_t>(a.nq, st);
+        order = scratch<int32_t>(a.nq, st);
         const bool morton = t.dims == 3 && knn_morton_order();
         int bits = 1;
         if (morton) {
             unsigned long long* box = nullptr;
-            KD_CUDA(cudaMallocAsync((void**)&box, 6 * sizeof(unsigned long long), st));
+            box = scratch<unsigned long long>(6, st);
             const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
             KD_CUDA(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, st));
             k_qbox<<<592, 256, 0, st>>>(a.queries, a.nq, box);
             k_morton<<<(unsigned)((a.nq + 255) / 256), 256, 0, st>>>(a.queries, a.nq, box, k0, v0);
-            cudaFreeAsync(box, st);
+            scratch_free(box, st);
             bits = 32;
         } else {
             const unsigned blocks = (unsigned)((a.nq + 1023) / 1024);  // 4 queries per thread
@@ -975,13 +1013,13 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
         }
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
-        KD_CUDA(cudaMallocAsync(&tmp, tb, st));
+        tmp = scratch<unsigned char>(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, order, (int)a.nq, 0, bits, st);
     }
     if (a.packet && knn_packet(t, a, order, st)) {
         if (order) {
-            cudaFreeAsync(k0, st); cudaFreeAsync(k1, st); cudaFreeAsync(v0, st); cudaFreeAsync(order, st);
-            cudaFreeAsync(tmp, st);
+            scratch_free(k0, st); scratch_free(k1, st); scratch_free(v0, st); scratch_free(order, st);
+            scratch_free(tmp, st);
         }
         return;
     }
@@ -991,8 +1029,8 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
     else dispatch_d<double>(t, a, order, home, st);
     KD_CUDA(cudaGetLastError());
     if (order) {
-        cudaFreeAsync(k0, st); cudaFreeAsync(k1, st); cudaFreeAsync(v0, st); cudaFreeAsync(order, st);
-        cudaFreeAsync(tmp, st);
+        scratch_free(k0, st); scratch_free(k1, st); scratch_free(v0, st); scratch_free(order, st);
+        scratch_free(tmp, st);
     }
 }
 
