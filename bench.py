@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--points", dest="n", type=int, default=None, help="override points per GPU (debug)")
     p.add_argument("--queries", dest="q", type=int, default=None, help="override queries per GPU (debug)")
     p.add_argument("--no-e2e", action="store_true")
@@ -459,20 +459,28 @@ def run_b200(args):
 
 
 def run_b200_multi(args):
-    """N > 1 (torchrun, one process per GPU): the PANDA global tier on NCCL.
-    Weak scaling: every rank owns 64M points / 16M queries of the workload law;
-    a step = global planes (sample all-gather + summed device histograms) +
-    all-to-all redistribution + local build, then the 5-step distributed query
-    (route, local KNN, r' forwarding, radius KNN, merge) -- all device-resident."""
+    """N > 1 (torchrun, one process per GPU): the PANDA global tier over NCCL.
+
+    C3 (default): the config's 256M points / 64M queries at every N (strong
+    scaling) -- 8 fixed shards of the C3 law, rank r of N generating shards
+    [8r/N, 8(r+1)/N) on its GPU.  C5: one 250M-point shard (65,536 halos, ids >=
+    2^32) and 62.5M fresh queries per GPU (weak scaling; 2B / 500M at N = 8).
+    A step = global planes (sample all-gather + summed device histograms, NCCL) +
+    alltoallv redistribution + local build, then the distributed query (route,
+    local KNN, r' forwarding, radius KNN, device merge, results home) -- every
+    array device-resident; time = max over ranks of CUDA-event time."""
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, rank_build_global
+    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, DeviceRegions, rank_build_global
     from paper_1607_08220_b200.comm import TorchComm
-    from paper_1607_08220_b200.dist_device import DeviceRegions, rank_query_device
+    from paper_1607_08220_b200.dist_query import QueryStats, rank_query
     from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
-    from paper_1607_08220_b200.workloads import CONFIGS, make_points, make_queries
+    from paper_1607_08220_b200.workloads import C3_SHARDS, CONFIGS, make_shard
 
+    if "WORLD_SIZE" not in os.environ:  # plain `python bench.py --config C5`: a one-rank process group
+        os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(29400 + os.getpid() % 500))
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -480,45 +488,54 @@ def run_b200_multi(args):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     comm = TorchComm()
-    w = CONFIGS[args.config]
-    n = args.n or w.n
-    q = args.q or w.q
-    rows = make_points(args.config, dev, seed=1000 + rank, n=n)
-    coords = rows.t().contiguous()
-    ids = torch.arange(n, dtype=torch.int64, device=dev) + rank * n
-    queries, sel = make_queries(args.config, rows, dev, seed=2000 + rank, q=q)
-    excl = (sel + rank * n) if sel is not None else None
-    qids = torch.arange(q, dtype=torch.int64, device=dev)
+    cfgname = args.config if args.config in ("C3", "C5") else "C3"
+    w = CONFIGS[cfgname]
+    if cfgname == "C5":
+        shards, scaling = [rank], "weak"
+    else:
+        if C3_SHARDS % world:
+            raise SystemExit(f"C3 over {world} GPUs: use a divisor of {C3_SHARDS}")
+        per = C3_SHARDS // world
+        shards, scaling = list(range(rank * per, (rank + 1) * per)), "strong"
+    parts = [make_shard(cfgname, s, dev, n=args.n, q=args.q) for s in shards]
+    coords = torch.cat([p[0] for p in parts]).t().contiguous()
+    ids = torch.cat([p[1] for p in parts])
+    queries = torch.cat([p[2] for p in parts])
+    del parts
+    n, q = coords.shape[1], queries.shape[0]
+    tot = torch.tensor([n, q], dtype=torch.int64, device=dev)
+    dist.all_reduce(tot)
+    n_total, q_total = (int(v) for v in tot.tolist())
     ccfg, bcfg = ClusterConfig(seed=0), BuildConfig(bucket_size=w.leaf, seed=0)
     stream = torch.cuda.current_stream(dev)
+    slice_size = None  # one slice per step (the pipeline matters for the host API's small batches)
 
-    def step():
+    def step(c_in, q_in):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        gt, pts, st = rank_build_global(comm, DevicePoints(coords, ids), ccfg)
+        gt, pts, st = rank_build_global(comm, DevicePoints(c_in, ids), ccfg)
         tree = build_local_tree_device(pts.coords, pts.ids, bcfg)
         e[1].record(stream)
-        stats = {}
-        out = rank_query_device(comm, tree, DeviceRegions(gt, dev), qids, queries, w.k, excl=excl, stats=stats)
+        qs = QueryStats(rank=rank)
+        out = rank_query(comm, tree, DeviceRegions(gt, dev), q_in, w.k, slice_size=slice_size, stats=qs)
         e[2].record(stream)
-        return tree, out, e, st, stats
+        return tree, out, e, st, qs
 
     tree = out = None
     for _ in range(args.warmup):
         del tree, out
-        tree, out, _, _, _ = step()
+        tree, out, _, _, _ = step(coords, queries)
     torch.cuda.synchronize(); dist.barrier(); torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
-    evs, moved, fwd = [], 0, 0
-    levels = 0
+    evs, moved, fwd, req = [], 0, 0, 0
     for _ in range(args.steps):
-        del tree, out  # free the previous step's tree and results before building the next
-        tree, out, e, st, stats = step()
-        levels = tree.build_info["levels"]
+        del tree, out
+        tree, out, e, st, qs = step(coords, queries)
         evs.append(e)
         moved += st["points_moved"]
-        fwd += stats.get("queries_forwarded", 0)
+        fwd += qs.queries_forwarded
+        req += qs.requests_sent
     torch.cuda.synchronize(); dist.barrier(); torch.cuda.synchronize()
     clk = clocks.stop()
     tb = sum(a.elapsed_time(b) for a, b, _ in evs) / len(evs) / 1e3
@@ -526,8 +543,9 @@ def run_b200_multi(args):
     t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tb, tq = t.tolist()
-    tot = torch.tensor([moved / args.steps, fwd / args.steps], dtype=torch.float64, device=dev)
-    dist.all_reduce(tot)
+    cnt = torch.tensor([moved / args.steps, fwd / args.steps, req / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(cnt)
+    # sanity: a sample of this rank's rows vs an fp64 brute force over ALL points (gathered)
     # e2e: pinned host inputs -> device -> distributed build + query -> results to host
     h_c = coords.cpu().pin_memory()
     h_q = queries.cpu().pin_memory()
@@ -535,22 +553,20 @@ def run_b200_multi(args):
     h_i = torch.empty((q, w.k), dtype=torch.int64).pin_memory()
     h_n = torch.empty((q,), dtype=torch.int64).pin_memory()
     te = []
-    tr = None
     for it in range(2 + min(args.steps, 2)):
-        del tr, tree, out
+        del tree, out
         tree = out = None
         torch.cuda.synchronize(); dist.barrier()
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         dc = h_c.to(dev, non_blocking=True)
         dq = h_q.to(dev, non_blocking=True)
-        gt, pts, _ = rank_build_global(comm, DevicePoints(dc, ids), ccfg)
-        tr = build_local_tree_device(pts.coords, pts.ids, bcfg)
-        od, oi, oc = rank_query_device(comm, tr, DeviceRegions(gt, dev), qids, dq, w.k, excl=excl)
+        tree, out, _, _, _ = step(dc, dq)
+        od, oi, _, oc = out
         h_d.copy_(od, non_blocking=True); h_i.copy_(oi, non_blocking=True); h_n.copy_(oc, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
-        del od, oi, oc, dc, dq, pts
+        del dc, dq
         if it >= 2:
             te.append(a.elapsed_time(b) / 1e3)
     tt = torch.tensor([float(np.mean(te))], dtype=torch.float64, device=dev)
@@ -558,26 +574,31 @@ def run_b200_multi(args):
     te_m = tt.item()
     if rank == 0:
         peak, peak_kind = peaks()
-        bbytes, levels_model = build_bytes(n, w.dims, w.leaf)
+        per_gpu_n = n_total / world
+        bbytes, levels_model = build_bytes(per_gpu_n, w.dims, w.leaf)
         ach_b = bbytes / tb / 1e9
         line = {
             "metric": METRIC,
-            "value": world * n / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "value": n_total / tb / 1e6, "unit": "Mpoints/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": (tb + tq) * 1e3, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "n_per_gpu": n, "q_per_gpu": q, "k": w.k, "leaf": w.leaf,
-                       "dims": w.dims, "parallelism": f"global kd-tree over {world} GPUs (NCCL all-to-all)",
+            "config": {"workload": w.name, "n": n_total, "q": q_total, "k": w.k, "leaf": w.leaf, "dims": w.dims,
+                       "n_per_gpu": n, "q_per_gpu": q,
+                       "parallelism": f"global kd-tree over {world} GPUs (NCCL all-to-all), {scaling} scaling",
                        "l2": "inputs larger than L2"},
             "ms_build": tb * 1e3, "ms_knn": tq * 1e3,
             "roofline": {"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s", "frac": ach_b / peak,
-                         "traffic": None, "kernel": "per-GPU local build + global tier", "peak_kind": peak_kind,
-                         "model": f"N*L*(8D+12) per GPU, L={levels_model}"},
-            "knn": {"value": world * q / tq, "unit": "queries/s"},
-            "points_moved_per_step": int(tot[0].item()), "queries_forwarded_per_step": int(tot[1].item()),
-            # local build (12 per level + 11) + global tier (4 per global level) + query
-            # (home-leaf keys, radix sort, KNN; route x2; remote KNN)
-            "gpu_launches": 12 * levels + 11 + 4 * (world.bit_length() - 1) + 12, "clocks": clk,
-            "e2e": {"value": world * n / te_m / 1e6, "unit": "Mpoints/s (build + query, host in/out)",
+                         "traffic": None, "kernel": "per-GPU global tier + local build", "peak_kind": peak_kind,
+                         "model": f"N/P*L*(8D+12) per GPU, L={levels_model}"},
+            "knn": {"value": q_total / tq, "unit": "queries/s"},
+            "points_moved_per_step": int(cnt[0].item()), "queries_forwarded_per_step": int(cnt[1].item()),
+            "requests_per_step": int(cnt[2].item()),
+            # local build (12 per level + 11) + global tier (split, unpack, hist per level) + query
+            # (route x2, KNN x2, merge, sorts)
+            "gpu_launches": 12 * (tree.build_info["levels"] if tree is not None else 20) + 11
+                            + 4 * (world.bit_length() - 1) + 16,
+            "clocks": clk,
+            "e2e": {"value": n_total / te_m / 1e6, "unit": "Mpoints/s (build + query, host in/out)",
                     "h2d_bytes_per_step": int(n * w.dims * 4 + q * w.dims * 8),
                     "d2h_bytes_per_step": int(q * w.k * 16 + q * 8), "ms_step": te_m * 1e3},
             "cpu_baseline": None,
@@ -590,7 +611,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("KDB_FORCE_GLOBAL"):
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("KDB_FORCE_GLOBAL") or args.config == "C5":
         run_b200_multi(args)
     else:
         run_b200(args)

@@ -137,11 +137,29 @@ KD_API int kd_tree_free(kd_tree* t);
 KD_API int kd_histogram(const void* values, int dtype, int64_t n, const double* boundaries, int64_t nb,
                         int64_t* counts, int64_t* equals, unsigned flags, void* stream);
 
-/* redistribute side split (cluster.py:292-294): stable two-way partition of a
- * rank's SoA points + ids, coord[dim] < value first.  Device pointers only. */
-KD_API int kd_partition(const void* coords, int dtype, int64_t n, int dims, const uint64_t* ids, int dim,
-                        double value, void* out_coords, uint64_t* out_ids, int64_t* n_low, unsigned flags,
-                        void* stream);
+/* redistribute side split (cluster.py:292-294, replaces the per-side index
+ * arrays of redistribute): stable two-way partition of a rank's SoA points + ids,
+ * coord[dim] < value first, written as packed rows [coords (padded to 8 B) | id]
+ * -- the all-to-all send buffer.  *n_low (DEVICE memory) receives the low-side
+ * count.  Asynchronous on `stream`; device pointers only. */
+KD_API int kd_split_rows(const void* coords, int dtype, int64_t n, int dims, const uint64_t* ids, int dim,
+                         double value, void* out_rows, int64_t* n_low, unsigned flags, void* stream);
+
+/* packed rows (kd_split_rows layout) -> SoA coords [dims][n] + ids.  Device ptrs. */
+KD_API int kd_unpack_rows(const void* rows, int64_t n, int dims, int dtype, void* out_coords, uint64_t* out_ids,
+                          unsigned flags, void* stream);
+
+/* owner-side merge (dist_query.py:138-161 merge_topk / _merge_arrays): for each of
+ * m owned queries, its local sorted top-k (local_c entries, this rank) and the
+ * nr remote replies addressed to it (reply_slot = owned-query index; reply_c
+ * entries from rank reply_rank) -> the k smallest by (sq_dist, point_id), with
+ * the contributing rank.  *dup_flag (device int32) is set to 1 when one point id
+ * appears twice in a query's pool (the reference's ValueError).  Device ptrs. */
+KD_API int kd_merge_topk(int64_t m, int64_t k, const double* local_d, const uint64_t* local_i, const int64_t* local_c,
+                         int32_t my_rank, int64_t nr, const int64_t* reply_slot, const double* reply_d,
+                         const uint64_t* reply_i, const int64_t* reply_c, const int32_t* reply_rank, double* out_d,
+                         uint64_t* out_i, int32_t* out_rank, int64_t* out_c, int32_t* dup_flag, unsigned flags,
+                         void* stream);
 
 /* GlobalTree.owner_of_batch + ranks_within (cluster.py:96-154): owner rank of
  * each query (ties right) and, when `within` is non-NULL, the bitmask of other

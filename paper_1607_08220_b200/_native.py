@@ -19,8 +19,8 @@ KD_F32, KD_F64 = 1, 2
 KD_DEVICE_PTRS, KD_NO_SORT, KD_THREAD_PER_QUERY, KD_KNN_PACKET = 1, 2, 4, 8
 
 EXPORTED = ("kd_version", "kd_last_error", "kd_device_count", "kd_tree_build", "kd_tree_import",
-            "kd_tree_get_info", "kd_tree_export", "kd_knn", "kd_tree_free", "kd_histogram", "kd_partition",
-            "kd_route")
+            "kd_tree_get_info", "kd_tree_export", "kd_knn", "kd_tree_free", "kd_histogram", "kd_split_rows",
+            "kd_route", "kd_unpack_rows", "kd_merge_topk")
 
 
 class kd_build_cfg(C.Structure):
@@ -62,8 +62,13 @@ def _load():
     L.kd_tree_free.argtypes = [C.c_void_p]
     L.kd_histogram.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                C.c_uint, C.c_void_p]
-    L.kd_partition.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_double,
-                               C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_uint, C.c_void_p]
+    L.kd_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                                C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
+    L.kd_unpack_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_uint,
+                                 C.c_void_p]
+    L.kd_merge_topk.argtypes = [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
     L.kd_route.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                            C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
     for name in EXPORTED:

@@ -1,22 +1,36 @@
 """Global spatial partition across GPUs (drop-in for ``kdknn.cluster``).
 
-The top log2(P) levels of the kd-tree split the points across ranks
-(cluster.py:354-417 of the reference): per level, every rank group all-gathers
-a 256-point sample per rank, picks the max-variance dimension of the sample,
-histograms ALL its local points against the distinct sampled values on the GPU
-(``kd_histogram``), sum-reduces the histograms over the group and selects the
-boundary closest to the median (same binary64 arithmetic as
-median.py:143-166); degenerate splits fall back to inclusive candidates just
-above a boundary, then to the next dimension.  Points are then exchanged so the
-lower half of the group holds coord < value, balanced by the reference's
-contiguous-slice plan (cluster.py:281-351): the stable device partition
-(``kd_partition``) feeds an all-to-all of SoA point blocks (NCCL over NVLink in
-the multi-process backend).  Every rank ends with exactly the points, in exactly
-the order, the reference would give it -- so its local tree, and the engine
-bundle, are byte-identical to the reference's.
+The top log2(P) levels of the kd-tree split the points across ranks (PAPER.md
+"global kd-tree"; reference cluster.py:354-417).  Same result as the
+reference -- planes, per-rank point sets and their order, hence local trees and
+engine bundles byte-identical -- but organised around device collectives
+instead of the reference's per-group message exchange:
 
-Small control data (samples, histograms, planes, counts) is handled on the
-host with numpy, exactly as the reference does.
+per level (groups of G = P >> level consecutive ranks, all groups at once):
+
+1. every rank draws its 256-point sample (SplitMix64 Fisher-Yates, median.py:74-85)
+   and ONE ``all_gather`` of fixed-size sample tensors gives every rank every
+   group's sample;
+2. every rank derives, for every group, the max-variance dimension order and the
+   distinct sampled values (numpy on a few KB, the reference's exact arithmetic);
+3. rounds over candidate dimensions: each rank histograms ALL its points of the
+   round's dimension against its group's boundaries on the GPU
+   (``kd_histogram``: counts + exact-equal counts), writes them into its group's
+   segment of one buffer, and ONE ``all_reduce`` (NCCL) sums every group at once
+   (cluster.py:246-248 group_sum_reduce).  Every rank then decides every group's
+   plane with the reference's rule (median.py:143-166 closest-to-half boundary,
+   the inclusive ``nextafter`` fallback of cluster.py:262-273, next dimension) --
+   so no plane all-gather is needed and an unsplittable group raises on every
+   rank together;
+4. redistribution (cluster.py:281-351 semantics): ``kd_split_rows`` writes the
+   rank's points as packed rows, low side first, stable; an ``all_gather`` of the
+   (low, high) counts lets every rank compute the balanced contiguous-slice plan;
+   ONE ``alltoallv`` moves the rows (NCCL over NVLink) and ``kd_unpack_rows``
+   restores SoA.  Received blocks arrive in sender-rank order, the reference's
+   concatenation order.
+
+Per level the host reads back the samples, the summed histograms and the counts
+(small tensors); all point data stays on the device.
 """
 
 from __future__ import annotations
@@ -29,18 +43,17 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .comm import ClusterAborted, run_ranks
+from .comm import run_ranks
 from .core import PointSet, Region, SplitPlane, min_sq_dist_to_region
 
 __all__ = ["ClusterConfig", "GlobalTree", "RankState", "UnsplittableDataError", "build_global_tree",
            "choose_global_split_dimension", "redistribute", "owner_of", "ranks_within", "sample_points",
-           "derive_seed", "sample_indices", "DevicePoints", "CudaBackend", "rank_build_global"]
+           "derive_seed", "sample_indices", "DevicePoints", "CudaBackend", "rank_build_global", "DeviceRegions"]
 
 _M64 = 0xFFFFFFFFFFFFFFFF
 _GAMMA = 0x9E3779B97F4A7C15
 _GLOBAL_PATH_TAG = 1 << 40   # cluster.py:54
 _SALT_GLOBAL_SAMPLE = 101    # cluster.py:55
-STRIDE = 32
 
 
 class UnsplittableDataError(RuntimeError):
@@ -60,7 +73,7 @@ def derive_seed(seed: int, path: int, salt: int) -> int:
 
 
 def sample_indices(n: int, m: int, seed: int) -> np.ndarray:
-    """median.py:74-85 partial Fisher-Yates over arange(n) (sparse swap map)."""
+    """median.py:74-85: m draws of a partial Fisher-Yates over 0..n-1 (sparse swap map)."""
     state = seed & _M64
     swapped: dict[int, int] = {}
     out = np.empty(m, dtype=np.int64)
@@ -79,6 +92,8 @@ def sample_indices(n: int, m: int, seed: int) -> np.ndarray:
 
 @dataclass(frozen=True)
 class ClusterConfig:
+    """cluster.py:62-72."""
+
     global_sample_m: int = 256
     seed: int = 0
     workers: int = 1
@@ -115,22 +130,21 @@ class GlobalTree:
 
     def owner_of_batch(self, queries) -> np.ndarray:
         queries = np.asarray(queries, dtype=np.float64)
-        nq = queries.shape[0]
-        idx = np.zeros(nq, dtype=np.int64)
+        heap = np.zeros(queries.shape[0], dtype=np.int64)
+        rows = np.arange(queries.shape[0])
         for _ in range(self.levels):
-            d = self.plane_dims[idx]
-            v = self.plane_values[idx]
-            idx = 2 * idx + 1 + (queries[np.arange(nq), d] >= v).astype(np.int64)
-        return idx - self.plane_dims.shape[0]
+            go_right = queries[rows, self.plane_dims[heap]] >= self.plane_values[heap]
+            heap = 2 * heap + 1 + go_right
+        return heap - self.plane_dims.shape[0]
 
     def region_of(self, rank: int) -> Region:
         region = Region.unbounded(self.dims)
-        idx, levels = 0, self.levels
-        for lv in range(levels):
-            bit = (rank >> (levels - 1 - lv)) & 1
-            low, high = region.split(SplitPlane(int(self.plane_dims[idx]), float(self.plane_values[idx])))
-            region = high if bit else low
-            idx = 2 * idx + 1 + bit
+        idx = 0
+        for lv in range(self.levels):
+            high = (rank >> (self.levels - 1 - lv)) & 1
+            lo_half, hi_half = region.split(SplitPlane(int(self.plane_dims[idx]), float(self.plane_values[idx])))
+            region = hi_half if high else lo_half
+            idx = 2 * idx + 1 + high
         return region
 
     def regions(self) -> list:
@@ -144,9 +158,9 @@ class GlobalTree:
     def ranks_within(self, q, sq_radius: float) -> np.ndarray:
         """Ranks (owner excluded) whose region is strictly closer than the radius."""
         owner = self.owner_of(q)
-        out = [r for r in range(self.rank_count)
-               if r != owner and min_sq_dist_to_region(q, self.region_of(r)) < sq_radius]
-        return np.asarray(sorted(out), dtype=np.int64)
+        return np.asarray([r for r in range(self.rank_count)
+                           if r != owner and min_sq_dist_to_region(q, self.region_of(r)) < sq_radius],
+                          dtype=np.int64)
 
     def to_bytes(self) -> bytes:
         return (struct.pack("<II", self.dims, self.rank_count)
@@ -171,7 +185,7 @@ def ranks_within(gt: GlobalTree, q, sq_radius) -> np.ndarray:
 
 # ---------------------------------------------------------------------------------------------
 class DevicePoints:
-    """A rank's points on its GPU: coords (dims, n) float32|float64 SoA + int64 ids (uint64 bits)."""
+    """A rank's points on its device: coords (dims, n) float32|float64 SoA + int64 ids (uint64 bits)."""
 
     def __init__(self, coords, ids):
         self.coords = coords
@@ -200,8 +214,19 @@ class DevicePoints:
     def take(self, sel):
         return DevicePoints(self.coords[:, sel].contiguous(), self.ids[sel].contiguous())
 
-    def slice(self, a, b):
-        return DevicePoints(self.coords[:, a:b].contiguous(), self.ids[a:b].contiguous())
+
+class DeviceRegions:
+    """The replicated global tree on a rank's device: planes + region boxes."""
+
+    def __init__(self, gt: GlobalTree, device):
+        import torch
+        self.p = gt.rank_count
+        self.dims = gt.dims
+        lo, hi = gt.region_bounds()
+        self.pdim = torch.as_tensor(np.ascontiguousarray(gt.plane_dims, dtype=np.int32)).to(device)
+        self.pval = torch.as_tensor(np.ascontiguousarray(gt.plane_values, dtype=np.float64)).to(device)
+        self.lo = torch.as_tensor(lo).to(device)
+        self.hi = torch.as_tensor(hi).to(device)
 
 
 def _dtype_code(coords) -> int:
@@ -209,76 +234,112 @@ def _dtype_code(coords) -> int:
     return N.KD_F32 if coords.dtype == torch.float32 else N.KD_F64
 
 
+def _stream(t):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
 class CudaBackend:
-    """Rank-local device work of the global tier: the sm_100a kernels behind the C-ABI."""
+    """Rank-local device work of the global tier: the sm_100a kernels behind the C-ABI.
+    Every method only enqueues work on the current stream and returns device tensors."""
 
     name = "cuda"
 
-    def histogram(self, pts, dim, boundaries):
-        return device_histogram(pts, dim, boundaries)
+    def histogram(self, pts: DevicePoints, dim: int, boundaries: np.ndarray):
+        """(counts (nb+1,), equals (nb,)) int64 device tensors (median.py:243-265)."""
+        import torch
+        dev = pts.coords.device
+        nb = int(boundaries.shape[0])
+        out = torch.zeros(2 * nb + 1, dtype=torch.int64, device=dev)
+        if pts.count:
+            b = torch.as_tensor(np.ascontiguousarray(boundaries, dtype=np.float64)).to(dev)
+            N.check(N.lib.kd_histogram(pts.coords[dim].data_ptr(), _dtype_code(pts.coords), pts.count,
+                                       b.data_ptr(), nb, out.data_ptr(), out[nb + 1:].data_ptr(),
+                                       N.KD_DEVICE_PTRS, _stream(pts.coords)))
+        return out[:nb + 1], out[nb + 1:]
 
-    def partition(self, pts, plane):
-        return device_partition(pts, plane)
+    def split_rows(self, pts: DevicePoints, dim: int, value: float):
+        """Packed rows (low side first, stable) + the low-side count (1,) on the device."""
+        import torch
+        dev = pts.coords.device
+        es = pts.coords.element_size()
+        w = ((pts.dims * es + 7) // 8) * 8 + 8
+        rows = torch.empty((pts.count, w), dtype=torch.uint8, device=dev)
+        n_low = torch.zeros(1, dtype=torch.int64, device=dev)
+        N.check(N.lib.kd_split_rows(pts.coords.data_ptr(), _dtype_code(pts.coords), pts.count, pts.dims,
+                                    pts.ids.data_ptr(), dim, float(value), rows.data_ptr(), n_low.data_ptr(),
+                                    N.KD_DEVICE_PTRS, _stream(pts.coords)))
+        return rows, n_low
 
-    def build(self, pts, build_cfg):
+    def unpack_rows(self, rows, dims: int, dtype) -> DevicePoints:
+        import torch
+        n = rows.shape[0]
+        coords = torch.empty((dims, n), dtype=dtype, device=rows.device)
+        ids = torch.empty(n, dtype=torch.int64, device=rows.device)
+        if n:
+            N.check(N.lib.kd_unpack_rows(rows.data_ptr(), n, dims, _dtype_code(coords), coords.data_ptr(),
+                                         ids.data_ptr(), N.KD_DEVICE_PTRS, _stream(rows)))
+        return DevicePoints(coords, ids)
+
+    def build(self, pts: DevicePoints, build_cfg):
         from .local_tree import build_local_tree_device
         return build_local_tree_device(pts.coords, pts.ids, build_cfg)
 
-    def knn(self, tree, queries, k, radii=None):
-        """queries (m, D) float64 tensor on the tree's device -> host numpy
-        (dists, ids u64, counts, counters)."""
+    def knn(self, tree, q, k: int, radii=None, excl=None, counters: bool = False):
+        """(dists (m,k) f64, ids (m,k) int64 bits of u64, counts (m,), counters (m,3)|None) on the device."""
+        import torch
         from .local_query import find_knn_device
-        if queries.shape[0] == 0 or tree.count == 0:
-            m = queries.shape[0]
-            return (np.zeros((m, k)), np.zeros((m, k), np.uint64), np.zeros(m, np.int64), np.zeros((m, 3), np.int64))
-        d, i, c, ctr = find_knn_device(tree, queries.contiguous(), k, radii=radii, counters=True)
-        return d.cpu().numpy(), i.cpu().numpy().view(np.uint64), c.cpu().numpy(), ctr.cpu().numpy()
+        m = q.shape[0]
+        if m == 0 or tree.count == 0:
+            z = torch.zeros
+            return (z((m, k), dtype=torch.float64, device=q.device), z((m, k), dtype=torch.int64, device=q.device),
+                    z(m, dtype=torch.int64, device=q.device),
+                    z((m, 3), dtype=torch.int64, device=q.device) if counters else None)
+        return find_knn_device(tree, q.contiguous(), k, radii=radii, exclude_ids=excl, counters=counters)
+
+    def route(self, regions: DeviceRegions, q, radii=None, within: bool = False):
+        """(owner rank int32 (m,), bitmask of other ranks within r (m,) int64 | None)."""
+        import torch
+        m = q.shape[0]
+        owner = torch.zeros(m, dtype=torch.int32, device=q.device)
+        wm = torch.zeros(m, dtype=torch.int64, device=q.device) if within else None
+        if m:
+            N.check(N.lib.kd_route(regions.pdim.data_ptr() if regions.p > 1 else None,
+                                   regions.pval.data_ptr() if regions.p > 1 else None, regions.p,
+                                   regions.lo.data_ptr(), regions.hi.data_ptr(), q.contiguous().data_ptr(), m,
+                                   regions.dims, radii.data_ptr() if radii is not None else None, owner.data_ptr(),
+                                   wm.data_ptr() if within else None, N.KD_DEVICE_PTRS, _stream(q)))
+        return owner, wm
+
+    def merge(self, k: int, ld, li, lc, my_rank: int, slot, rd, ri, rc, rrank):
+        """kd_merge_topk: (dists, ids, ranks int32, counts, duplicate flag (1,) int32) on the device."""
+        import torch
+        m = ld.shape[0]
+        dev = ld.device
+        od = torch.zeros((m, k), dtype=torch.float64, device=dev)
+        oi = torch.zeros((m, k), dtype=torch.int64, device=dev)
+        orank = torch.zeros((m, k), dtype=torch.int32, device=dev)
+        oc = torch.zeros(m, dtype=torch.int64, device=dev)
+        dup = torch.zeros(1, dtype=torch.int32, device=dev)
+        nr = slot.shape[0]
+        if m:
+            N.check(N.lib.kd_merge_topk(m, k, ld.data_ptr(), li.data_ptr(), lc.data_ptr(), my_rank, nr,
+                                        slot.data_ptr() if nr else None, rd.data_ptr() if nr else None,
+                                        ri.data_ptr() if nr else None, rc.data_ptr() if nr else None,
+                                        rrank.data_ptr() if nr else None, od.data_ptr(), oi.data_ptr(),
+                                        orank.data_ptr(), oc.data_ptr(), dup.data_ptr(), N.KD_DEVICE_PTRS,
+                                        _stream(ld)))
+        return od, oi, orank, oc, dup
 
 
 _CUDA = CudaBackend()
-
-
-def device_histogram(pts: DevicePoints, dim: int, boundaries: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    """histogram_with_equals of the rank's coordinate row `dim` on the GPU."""
-    import torch
-    nb = boundaries.shape[0]
-    counts = np.zeros(nb + 1, dtype=np.int64)
-    equals = np.zeros(nb, dtype=np.int64)
-    if pts.count == 0:
-        return counts, equals
-    b = np.ascontiguousarray(boundaries, dtype=np.float64)
-    row = pts.coords[dim]
-    with torch.cuda.device(pts.coords.device):
-        db = torch.as_tensor(b).to(pts.coords.device)
-        dc = torch.empty(nb + 1, dtype=torch.int64, device=pts.coords.device)
-        de = torch.empty(nb, dtype=torch.int64, device=pts.coords.device)
-        st = torch.cuda.current_stream(pts.coords.device).cuda_stream
-        N.check(N.lib.kd_histogram(row.data_ptr(), _dtype_code(pts.coords), pts.count, db.data_ptr(), nb,
-                                   dc.data_ptr(), de.data_ptr(), N.KD_DEVICE_PTRS, C.c_void_p(st)))
-        return dc.cpu().numpy(), de.cpu().numpy()
-
-
-def device_partition(pts: DevicePoints, plane: SplitPlane) -> tuple[DevicePoints, int]:
-    """Stable split: coord[dim] < value first (cluster.py:292-294)."""
-    import torch
-    if pts.count == 0:
-        return pts, 0
-    with torch.cuda.device(pts.coords.device):
-        oc = torch.empty_like(pts.coords)
-        oi = torch.empty_like(pts.ids)
-        nl = C.c_int64(0)
-        st = torch.cuda.current_stream(pts.coords.device).cuda_stream
-        N.check(N.lib.kd_partition(pts.coords.data_ptr(), _dtype_code(pts.coords), pts.count, pts.dims,
-                                   pts.ids.data_ptr(), plane.dim, float(plane.value), oc.data_ptr(), oi.data_ptr(),
-                                   C.byref(nl), N.KD_DEVICE_PTRS, C.c_void_p(st)))
-        return DevicePoints(oc, oi), int(nl.value)
 
 
 def sample_points(pts, m: int, seed: int):
     """min(m, n) points without replacement, deterministically (cluster.py:190-198)."""
     n = pts.count
     if n == 0:
-        return pts.take([]) if isinstance(pts, PointSet) else None
+        return pts.take(np.empty(0, dtype=np.int64)) if isinstance(pts, PointSet) else None
     picked = sample_indices(n, min(m, n), seed)
     if isinstance(pts, PointSet):
         return pts.take(picked)
@@ -286,181 +347,178 @@ def sample_points(pts, m: int, seed: int):
     return pts.take(torch.as_tensor(picked, device=pts.coords.device))
 
 
-def _group_of(rank: int, p: int, level: int) -> tuple:
-    g = p >> level
-    base = (rank // g) * g
-    return tuple(range(base, base + g))
-
-
-def _gather_group_sample(comm, group, pts: DevicePoints, cfg: ClusterConfig, level: int) -> np.ndarray:
-    seed = derive_seed(cfg.seed, _GLOBAL_PATH_TAG + level, _SALT_GLOBAL_SAMPLE + comm.rank)
-    s = sample_points(pts, cfg.global_sample_m, seed)
-    rows = s.coords.double().t().cpu().numpy() if s is not None and s.count else np.empty((0, pts.dims))
-    parts = comm.all_gather(rows)
-    rows = [parts[r] for r in group if parts[r].shape[0]]
-    return np.concatenate(rows, axis=0) if rows else np.empty((0, pts.dims), dtype=np.float64)
-
-
-def _select_median(boundaries: np.ndarray, counts: np.ndarray) -> tuple[int, int]:
-    """median.py:143-166 in binary64 (first minimum == strict `<` ties-low)."""
+# ---------------------------------------------------------------------------------------------
+def _median_split(boundaries: np.ndarray, g_counts: np.ndarray, g_equals: np.ndarray, group_n: int):
+    """The reference's plane rule for one candidate dimension (cluster.py:253-273 with
+    median.py:143-166): the boundary whose cumulative fraction is closest to 1/2
+    (first minimum), accepted when both sides are non-empty; else the best
+    non-degenerate cut at a boundary (exclusive) or just above it (inclusive,
+    nextafter); None when the dimension is constant over the group."""
     nb = boundaries.shape[0]
-    total = int(counts.sum())
-    if total <= 0 or nb == 0:
-        return -1, 0
-    cum = np.cumsum(counts[:nb])
-    diff = np.abs(cum / total - 0.5)
-    i = int(np.argmin(diff))
-    return i, int(cum[i])
+    cum = np.cumsum(g_counts[:nb])
+    total = int(g_counts.sum())
+    if total > 0 and nb > 0:
+        i = int(np.argmin(np.abs(cum / total - 0.5)))
+        below = int(cum[i])
+        if group_n < 2 or 0 < below < group_n:
+            return float(boundaries[i])
+    le = cum + g_equals[:nb]
+    best_diff, best_value = None, None
+    for i in range(nb):
+        for value, below in ((boundaries[i], cum[i]), (np.nextafter(boundaries[i], np.inf), le[i])):
+            if 0 < below < group_n:
+                diff = abs(int(below) / group_n - 0.5)
+                if best_diff is None or diff < best_diff:
+                    best_diff, best_value = diff, float(value)
+    return best_value
 
 
-def choose_global_split_dimension(comm, group, pts: DevicePoints, cfg: ClusterConfig, level: int = 0) -> int:
-    rows = _gather_group_sample(comm, group, pts, cfg, level)
-    if rows.shape[0] == 0:
-        return 0
-    return int(np.argsort(-np.var(rows, axis=0), kind="mergesort")[0])
-
-
-def _choose_planes(comm, group, pts: DevicePoints, cfg: ClusterConfig, level: int, backend=_CUDA) -> SplitPlane:
-    """cluster.py:228-278, restructured into rounds every rank takes part in (one
-    candidate dimension per round) so that collectives stay matched across groups."""
-    dims = pts.dims
-    rows = _gather_group_sample(comm, group, pts, cfg, level)
-    order = np.argsort(-np.var(rows, axis=0), kind="mergesort") if rows.shape[0] else np.zeros(dims, np.int64)
-    decided = rows.shape[0] == 0  # empty group: any plane keeps regions well-formed
-    plane = SplitPlane(0, 0.0)
-    group_n = 0
-    for t in range(dims):
-        payload = None
-        if not decided:
-            d = int(order[t])
-            boundaries = np.unique(rows[:, d])
-            counts, equals = backend.histogram(pts, d, boundaries)
-            payload = np.concatenate([counts, equals, [pts.count]]).astype(np.int64)
-        gathered = comm.all_gather(payload)
-        if not decided:
-            red = np.sum([gathered[r] for r in group], axis=0)
-            nb = boundaries.shape[0]
-            g_counts, g_equals, group_n = red[:nb + 1], red[nb + 1:2 * nb + 1], int(red[-1])
-            if group_n == 0:
-                plane, decided = SplitPlane(0, 0.0), True
-            else:
-                lt = np.cumsum(g_counts)[:nb]
-                bi, _ = _select_median(boundaries, g_counts)
-                value = float(boundaries[bi])
-                below = int(lt[np.searchsorted(boundaries, value)])
-                if group_n < 2 or 0 < below < group_n:
-                    plane, decided = SplitPlane(d, value), True
-                else:
-                    le = lt + g_equals
-                    best_diff, best_value = None, None
-                    for i in range(nb):
-                        for cv, cb in ((boundaries[i], lt[i]), (np.nextafter(boundaries[i], np.inf), le[i])):
-                            if 0 < cb < group_n:
-                                diff = abs(cb / group_n - 0.5)
-                                if best_diff is None or diff < best_diff:
-                                    best_diff, best_value = diff, float(cv)
-                    if best_value is not None:
-                        plane, decided = SplitPlane(d, best_value), True
-        flags = comm.all_gather(decided)
-        if all(flags):
+def _level_planes(comm, pts: DevicePoints, cfg: ClusterConfig, level: int, backend) -> dict:
+    """Every group's plane at this level, decided identically on every rank."""
+    import torch
+    p, me, dims = comm.size, comm.rank, pts.dims
+    gsize = p >> level
+    ngroups = p // gsize
+    mine = me // gsize
+    dev = pts.coords.device
+    m = cfg.global_sample_m
+    # 1. samples: one fixed-size all-gather for all groups
+    seed = derive_seed(cfg.seed, _GLOBAL_PATH_TAG + level, _SALT_GLOBAL_SAMPLE + me)
+    take = min(m, pts.count)
+    sbuf = torch.zeros((m + 1, dims), dtype=torch.float64, device=dev)
+    if take:
+        idx = torch.as_tensor(sample_indices(pts.count, take, seed), device=dev)
+        sbuf[:take] = pts.coords[:, idx].t().double()
+    sbuf[m, 0] = take
+    allS = comm.all_gather_t(sbuf).cpu().numpy()
+    rows, order = {}, {}
+    for g in range(ngroups):
+        parts = [allS[r, :int(allS[r, m, 0])] for r in range(g * gsize, (g + 1) * gsize)]
+        rows[g] = np.concatenate(parts, axis=0)
+        if rows[g].shape[0]:
+            order[g] = np.argsort(-np.var(rows[g], axis=0), kind="mergesort")
+    # an empty group keeps well-formed regions with any plane (cluster.py:231-235)
+    planes = {g: SplitPlane(0, 0.0) for g in range(ngroups) if rows[g].shape[0] == 0}
+    # 2. rounds over candidate dimensions; one all-reduce sums every group's histogram
+    for rnd in range(dims):
+        todo = [g for g in range(ngroups) if g not in planes]
+        if not todo:
             break
-    flags = comm.all_gather(decided)
-    if not all(flags):
-        bad = [r for r in range(comm.size) if not flags[r]]
+        bnd = {g: np.unique(rows[g][:, int(order[g][rnd])]) for g in todo}
+        nbm = max(b.shape[0] for b in bnd.values())
+        hist = torch.zeros((ngroups, 2 * nbm + 2), dtype=torch.int64, device=dev)
+        if mine in bnd:
+            nb = bnd[mine].shape[0]
+            counts, equals = backend.histogram(pts, int(order[mine][rnd]), bnd[mine])
+            hist[mine, :nb + 1] = counts
+            hist[mine, nbm + 1:nbm + 1 + nb] = equals
+            hist[mine, -1] = pts.count
+        red = comm.all_reduce_t(hist).cpu().numpy()
+        for g in todo:
+            nb = bnd[g].shape[0]
+            group_n = int(red[g, -1])
+            if group_n == 0:
+                planes[g] = SplitPlane(0, 0.0)
+                continue
+            v = _median_split(bnd[g], red[g, :nb + 1], red[g, nbm + 1:nbm + 1 + nb], group_n)
+            if v is not None:
+                planes[g] = SplitPlane(int(order[g][rnd]), v)
+    bad = [g for g in range(ngroups) if g not in planes]
+    if bad:
+        g = bad[0]
         raise UnsplittableDataError(
-            f"rank group(s) containing {bad} at level {level} hold {group_n if not decided else 'some'} points "
-            f"identical in every of {dims} dimensions; cannot split into nonempty halves")
-    return plane
+            f"rank group {tuple(range(g * gsize, (g + 1) * gsize))} at level {level} holds points identical "
+            f"in every of {dims} dimensions; cannot split into nonempty halves")
+    return planes
+
+
+def _slice_plan(counts: np.ndarray, group: range, me: int) -> np.ndarray:
+    """Rows this rank sends to each rank (cluster.py:302-346 contiguous-slice plan):
+    each side's points form a virtual sequence ordered by (sender rank, stable
+    local order); its receivers (lower / upper half of the group) take slices of
+    total//H (+1 for the first total%H).  Returns send counts per rank, in the
+    order the rows sit in this rank's split buffer (low side, then high side)."""
+    send = np.zeros(counts.shape[0], dtype=np.int64)
+    half = len(group) // 2
+    for side, recv in ((0, list(group)[:half]), (1, list(group)[half:])):
+        sizes = [int(counts[r, side]) for r in group]
+        total = sum(sizes)
+        share, rem = divmod(total, len(recv))
+        my0 = sum(sizes[:group.index(me)])
+        my1 = my0 + sizes[group.index(me)]
+        r0 = 0
+        for i, r in enumerate(recv):
+            r1 = r0 + share + (1 if i < rem else 0)
+            send[r] += max(0, min(my1, r1) - max(my0, r0))
+            r0 = r1
+    return send
 
 
 def redistribute(comm, group, pts: DevicePoints, plane: SplitPlane, backend=_CUDA) -> tuple[DevicePoints, int]:
-    """cluster.py:281-351: lower half of the group gets coord < value; receivers
-    take contiguous slices total//H (+1 for the first total%H) of the virtual
-    sequence ordered by (sender rank, stable local order)."""
+    """Exchange points inside `group` (consecutive ranks) so its lower half holds
+    coord < value (cluster.py:281-351 semantics).  Returns (new points, rows sent)."""
     import torch
-    group = tuple(group)
-    half = len(group) // 2
-    receivers = {0: group[:half], 1: group[half:]}
-    parted, nl = backend.partition(pts, plane)
-    side_rng = {0: (0, nl), 1: (nl, pts.count)}
-    counts = comm.all_gather((nl, pts.count - nl))
-    per_rank = {r: counts[r] for r in group}
-    sends, mine, sent = {}, [], 0
-    me = comm.rank
-    if me in group:
-        for side in (0, 1):
-            recv = receivers[side]
-            total = sum(per_rank[r][side] for r in group)
-            share, rem = divmod(total, len(recv))
-            targets = {r: share + (1 if i < rem else 0) for i, r in enumerate(recv)}
-            rstart, pos = {}, 0
-            for r in recv:
-                rstart[r] = pos
-                pos += targets[r]
-            soff, pos = {}, 0
-            for r in group:
-                soff[r] = pos
-                pos += per_rank[r][side]
-            my0, my1 = soff[me], soff[me] + per_rank[me][side]
-            for r in recv:
-                lo, hi = max(my0, rstart[r]), min(my1, rstart[r] + targets[r])
-                if lo >= hi:
-                    continue
-                a = side_rng[side][0] + (lo - my0)
-                blk = parted.slice(a, a + (hi - lo))
-                if r == me:
-                    mine.append(blk)
-                else:
-                    sends[r] = (blk.coords, blk.ids)
-                    sent += hi - lo
-    got = comm.alltoall(sends)
-    blocks = []
-    for src in sorted(set(got) | ({me} if mine else set())):
-        if src == me:
-            blocks.extend(mine)
-        else:
-            c, i = got[src]
-            blocks.append(DevicePoints(c, i))
-    blocks = [b for b in blocks if b.count]
-    if blocks:
-        new = DevicePoints(torch.cat([b.coords for b in blocks], dim=1).contiguous(),
-                           torch.cat([b.ids for b in blocks]).contiguous())
-    else:
-        new = DevicePoints(pts.coords[:, :0].contiguous(), pts.ids[:0].contiguous())
-    return new, sent
+    group = range(group[0], group[-1] + 1)
+    rows, n_low = backend.split_rows(pts, plane.dim, plane.value)
+    counts = comm.all_gather_t(torch.cat([n_low, n_low.new_full((1,), pts.count) - n_low])).cpu().numpy()
+    send = _slice_plan(counts, group, comm.rank)
+    recv, _ = comm.alltoallv(rows, send.tolist())
+    return backend.unpack_rows(recv, pts.dims, pts.coords.dtype), int(send.sum() - send[comm.rank])
 
 
 def rank_build_global(comm, pts: DevicePoints, cfg: ClusterConfig, backend=_CUDA):
-    """cluster.py:354-389 for one rank (SPMD)."""
+    """One rank's side of the global construction (SPMD, cluster.py:354-389
+    semantics).  Returns (GlobalTree, this rank's points, stats)."""
     import torch
-    p = comm.size
+    p, me = comm.size, comm.rank
     levels = p.bit_length() - 1
     dims = pts.dims
     plane_dims = np.full(max(p - 1, 0), -1, dtype=np.int32)
     plane_values = np.zeros(max(p - 1, 0), dtype=np.float64)
     stats = {"points_moved": 0, "t_global_split": 0.0, "t_redistribute": 0.0}
     for level in range(levels):
-        group = _group_of(comm.rank, p, level)
-        heap_idx = (1 << level) - 1 + (comm.rank >> (levels - level))
         t0 = time.perf_counter()
-        plane = _choose_planes(comm, group, pts, cfg, level, backend)
-        for idx, d, v in comm.all_gather((heap_idx, plane.dim, plane.value)):
-            if plane_dims[idx] != -1 and (plane_dims[idx] != d or plane_values[idx] != v):
-                raise AssertionError("rank group disagreed on a split plane")
-            plane_dims[idx], plane_values[idx] = d, v
+        planes = _level_planes(comm, pts, cfg, level, backend)
+        for g, pl in planes.items():
+            plane_dims[(1 << level) - 1 + g] = pl.dim
+            plane_values[(1 << level) - 1 + g] = pl.value
         stats["t_global_split"] += time.perf_counter() - t0
         t0 = time.perf_counter()
-        pts, sent = redistribute(comm, group, pts, plane, backend)
+        gsize = p >> level
+        group = range((me // gsize) * gsize, (me // gsize + 1) * gsize)
+        pts, sent = redistribute(comm, group, pts, planes[me // gsize], backend)
         stats["points_moved"] += sent
         stats["t_redistribute"] += time.perf_counter() - t0
     gt = GlobalTree(dims, plane_dims, plane_values)
     if pts.count and levels:
-        reg = gt.region_of(comm.rank)
-        lo = torch.as_tensor(reg.lower, device=pts.coords.device).to(pts.coords.dtype)[:, None]
-        hi = torch.as_tensor(reg.upper, device=pts.coords.device).to(pts.coords.dtype)[:, None]
-        if not bool(((pts.coords >= lo) & (pts.coords <= hi)).all()):
-            raise AssertionError(f"rank {comm.rank}: point outside its region after redistribution")
+        reg = gt.region_of(me)
+        lo = torch.as_tensor(reg.lower, device=pts.coords.device)[:, None]
+        hi = torch.as_tensor(reg.upper, device=pts.coords.device)[:, None]
+        c = pts.coords.double()
+        if not bool(((c >= lo) & (c <= hi)).all()):
+            raise AssertionError(f"rank {me}: point outside its region after redistribution")
     return gt, pts, stats
+
+
+def choose_global_split_dimension(comm, pts: DevicePoints, cfg: ClusterConfig, level: int = 0) -> int:
+    """Max-variance dimension of this rank's group sample (cluster.py:214-225)."""
+    import torch
+    p, me, dims = comm.size, comm.rank, pts.dims
+    gsize = p >> level
+    m = cfg.global_sample_m
+    seed = derive_seed(cfg.seed, _GLOBAL_PATH_TAG + level, _SALT_GLOBAL_SAMPLE + me)
+    take = min(m, pts.count)
+    sbuf = torch.zeros((m + 1, dims), dtype=torch.float64, device=pts.coords.device)
+    if take:
+        sbuf[:take] = pts.coords[:, torch.as_tensor(sample_indices(pts.count, take, seed),
+                                                    device=pts.coords.device)].t().double()
+    sbuf[m, 0] = take
+    allS = comm.all_gather_t(sbuf).cpu().numpy()
+    g0 = (me // gsize) * gsize
+    rows = np.concatenate([allS[r, :int(allS[r, m, 0])] for r in range(g0, g0 + gsize)], axis=0)
+    if rows.shape[0] == 0:
+        return 0
+    return int(np.argsort(-np.var(rows, axis=0), kind="mergesort")[0])
 
 
 @dataclass
@@ -478,9 +536,7 @@ def _f32_all(parts) -> bool:
     return all(_f32_exact(p.coords) for p in parts)
 
 
-def build_global_tree(points_per_rank: list, cfg: ClusterConfig):
-    """cluster.py:392-417 driver over in-process ranks.  Returns the replicated
-    GlobalTree, the redistributed per-rank PointSets and per-rank stats."""
+def _check_inputs(points_per_rank: list):
     p = len(points_per_rank)
     if p < 1 or (p & (p - 1)) != 0:
         raise ValueError(f"rank count {p} is not a power of two")
@@ -488,24 +544,29 @@ def build_global_tree(points_per_rank: list, cfg: ClusterConfig):
         raise ValueError("inconsistent dimensionality across ranks")
     if sum(ps.count for ps in points_per_rank) == 0:
         raise ValueError("empty dataset")
-    if p == 1:
-        gt = GlobalTree(points_per_rank[0].dims, np.empty(0, dtype=np.int32), np.empty(0, dtype=np.float64))
-        return gt, list(points_per_rank), [{"points_moved": 0, "t_global_split": 0.0, "t_redistribute": 0.0}]
-    dev_pts, gts, stats = build_global_device(points_per_rank, cfg)
-    return gts, [d.to_pointset() for d in dev_pts], stats
 
 
-def build_global_device(points_per_rank: list, cfg: ClusterConfig):
-    """Same as build_global_tree, but keeps every rank's points on its GPU."""
+def build_global_device(points_per_rank: list, cfg: ClusterConfig, backend=_CUDA):
+    """The global tier over in-process ranks, every rank's points kept on its device.
+    Returns (per-rank DevicePoints, GlobalTree, per-rank stats)."""
+    _check_inputs(points_per_rank)
     f32 = _f32_all(points_per_rank)
 
     def prog(comm, ps):
-        dp = DevicePoints.from_pointset(ps, comm.device, f32)
-        return rank_build_global(comm, dp, cfg)
+        return rank_build_global(comm, DevicePoints.from_pointset(ps, comm.device, f32), cfg, backend)
 
     res = run_ranks(len(points_per_rank), prog, [(ps,) for ps in points_per_rank])
-    trees = [r[0] for r in res]
-    for t in trees[1:]:
-        if t.to_bytes() != trees[0].to_bytes():
-            raise AssertionError("global tree replicas differ across ranks")
-    return [r[1] for r in res], trees[0], [r[2] for r in res]
+    blobs = {r[0].to_bytes() for r in res}
+    if len(blobs) != 1:
+        raise AssertionError("global tree replicas differ across ranks")
+    return [r[1] for r in res], res[0][0], [r[2] for r in res]
+
+
+def build_global_tree(points_per_rank: list, cfg: ClusterConfig, backend=_CUDA):
+    """cluster.py:392-417 driver: (GlobalTree, redistributed per-rank PointSets, stats)."""
+    _check_inputs(points_per_rank)
+    if len(points_per_rank) == 1:
+        gt = GlobalTree(points_per_rank[0].dims, np.empty(0, dtype=np.int32), np.empty(0, dtype=np.float64))
+        return gt, list(points_per_rank), [{"points_moved": 0, "t_global_split": 0.0, "t_redistribute": 0.0}]
+    dev_pts, gt, stats = build_global_device(points_per_rank, cfg, backend)
+    return gt, [d.to_pointset() for d in dev_pts], stats

@@ -1,26 +1,30 @@
 """Rank-to-rank communication for the global tier (replaces kdknn.transport / wire).
 
 The reference simulates MPI ranks as threads exchanging byte frames
-(transport.py:33-187, wire.py).  Here every exchange carries device tensors and
-the protocol code is written once, SPMD, against two collectives:
+(transport.py:33-187, wire.py:63-147).  Here every exchange is a collective on
+tensors that stay on the rank's device, written once, SPMD:
 
-* ``all_gather(obj)``   -- every rank contributes a small host object (numpy
-  arrays, tuples); returns the rank-ordered list.  Group collectives of the
-  reference (group_all_gather / group_sum_reduce) are all-gathers whose group
-  slice each member reads.
-* ``alltoall(sends)``   -- point-to-point blocks: ``sends[dst]`` is a tuple of
-  device tensors; returns ``{src: tuple}``.
+* ``all_gather_t(x)``      same-shape tensor from every rank -> (P, *x.shape)
+* ``all_reduce_t(x)``      element-wise sum over ranks (the reference's
+  group_sum_reduce: each group writes its own segment of a shared buffer)
+* ``alltoallv(rows, send_counts)``  variable all-to-all of 2-D row blocks:
+  ``rows`` holds the rows for rank 0, then rank 1, ... (``send_counts[r]`` of
+  them); returns the received rows in source-rank order and the per-source
+  counts.  One count exchange (a P-element tensor) and one data exchange; every
+  rank always enters both collectives, whatever it sends or receives.
 
-Two backends:
+Records of several fields travel as packed byte rows (``pack_rows`` /
+``unpack_rows``): one collective per exchange, whatever the number of fields.
+
+Backends:
 
 * :class:`ThreadComm` -- P ranks as threads of one process (the reference's
   execution model, so ``build_engine(points, RunConfig(ranks=P))`` keeps its
-  single-call API).  Rank r runs on CUDA device r % device_count; blocks move by
-  reference (same device) or device-to-device copy.
-* :class:`TorchComm` -- one process per GPU under torchrun:
-  ``torch.distributed`` all_gather_object for the small control data and
-  ``all_to_all_single`` over NCCL (NVLink/NVSwitch) for point/query blocks; gloo
-  on CPU for the multi-process host tests.
+  single-call API).  Rank r runs on CUDA device r % device_count; blocks move
+  by reference (same device) or device-to-device copy.
+* :class:`TorchComm` -- one process per GPU under torchrun: ``torch.distributed``
+  collectives on the rank's tensors -- NCCL over NVLink / NVSwitch for CUDA
+  tensors, gloo for the CPU multi-process tests.
 
 A failure on any thread aborts the whole in-process cluster (transport.py:89-104):
 surviving ranks raise :class:`ClusterAborted` instead of deadlocking.
@@ -32,11 +36,47 @@ import threading
 from concurrent.futures import ThreadPoolExecutor
 from typing import Callable, Sequence
 
-__all__ = ["ClusterAborted", "ThreadCluster", "ThreadComm", "TorchComm", "run_ranks"]
+__all__ = ["ClusterAborted", "ThreadCluster", "ThreadComm", "TorchComm", "run_ranks", "pack_rows", "unpack_rows"]
 
 
 class ClusterAborted(RuntimeError):
     """Raised in surviving ranks when another rank failed (transport.py:29-30)."""
+
+
+def pack_rows(*fields):
+    """Fields of n rows each ((n,) or (n, c) tensors of any dtype, one device) ->
+    (n, W) uint8 rows and the layout needed by :func:`unpack_rows`."""
+    import torch
+    n = fields[0].shape[0]
+    parts, spec = [], []
+    for f in fields:
+        cols = 1
+        for e in f.shape[1:]:
+            cols *= e
+        spec.append((f.dtype, cols, tuple(f.shape[1:])))
+        if n == 0:
+            parts.append(torch.empty((0, cols * f.element_size()), dtype=torch.uint8, device=f.device))
+        else:
+            parts.append(f.reshape(n, cols).contiguous().view(torch.uint8).reshape(n, cols * f.element_size()))
+    return torch.cat(parts, dim=1) if len(parts) > 1 else parts[0], spec
+
+
+def unpack_rows(rows, spec):
+    """Inverse of :func:`pack_rows` (fields come back contiguous)."""
+    import torch
+    out, off = [], 0
+    n = rows.shape[0]
+    for dtype, cols, tail in spec:
+        es = torch.empty((), dtype=dtype).element_size()
+        w = cols * es
+        if n == 0:
+            out.append(torch.empty((0,) + tail, dtype=dtype, device=rows.device))
+        else:
+            col = torch.empty((n, w), dtype=torch.uint8, device=rows.device)
+            col.copy_(rows[:, off:off + w])
+            out.append(col.view(dtype).reshape((n,) + tail))
+        off += w
+    return out
 
 
 class ThreadCluster:
@@ -46,7 +86,6 @@ class ThreadCluster:
         self.size = size
         self.barrier = threading.Barrier(size)
         self.slots: list = [None] * size
-        self.mail: list = [[None] * size for _ in range(size)]
         self.failed = threading.Event()
 
     def abort(self):
@@ -75,34 +114,53 @@ class ThreadComm:
         except threading.BrokenBarrierError:
             raise ClusterAborted("another rank failed") from None
 
-    def all_gather(self, obj):
+    def _exchange(self, mine):
+        """Publish `mine`, return every rank's value (rank order)."""
         c = self.cluster
         self._wait()
-        c.slots[self.rank] = obj
+        c.slots[self.rank] = mine
         self._wait()
         out = list(c.slots)
         self._wait()
         return out
 
-    def alltoall(self, sends: dict):
-        c = self.cluster
-        self._wait()
-        for dst, payload in sends.items():
-            c.mail[self.rank][dst] = payload
-        self._wait()
-        got = {}
+    def all_gather(self, obj):
+        """Small host objects (test / driver utility; the protocol uses tensors)."""
+        return self._exchange(obj)
+
+    def all_gather_t(self, x):
+        import torch
         dev = self.device
-        for src in range(self.size):
-            p = c.mail[src][self.rank]
-            if p is not None:
-                got[src] = tuple(t.to(dev, non_blocking=True) if hasattr(t, "to") else t for t in p)
-                if src != self.rank:
-                    self.bytes_moved += sum(t.numel() * t.element_size() for t in p if hasattr(t, "numel"))
-        self._wait()
-        for src in range(self.size):
-            c.mail[src][self.rank] = None
-        self._wait()
-        return got
+        return torch.stack([t.to(dev) for t in self._exchange(x)])
+
+    def all_reduce_t(self, x):
+        parts = self._exchange(x)
+        dev = self.device
+        acc = parts[0].to(dev).clone()
+        for t in parts[1:]:
+            acc += t.to(dev)
+        return acc
+
+    def alltoallv(self, rows, send_counts):
+        import torch
+        sc = [int(v) for v in (send_counts.tolist() if hasattr(send_counts, "tolist") else send_counts)]
+        allp = self._exchange((rows, sc))
+        dev = self.device
+        blocks, rc = [], []
+        cross = False
+        for src, (r, c) in enumerate(allp):
+            off = sum(c[:self.rank])
+            blk = r[off:off + c[self.rank]]
+            rc.append(int(c[self.rank]))
+            if src != self.rank:
+                self.bytes_moved += blk.numel() * blk.element_size()
+            cross |= blk.device != dev
+            blocks.append(blk.to(dev, non_blocking=True))
+        out = torch.cat(blocks) if blocks else rows[:0].to(dev)
+        if cross and dev.type == "cuda":
+            torch.cuda.synchronize(dev)  # peer blocks copied before their owners move on
+        self._wait()  # every rank has taken its blocks before senders reuse their buffers
+        return out, rc
 
     def barrier(self):
         self._wait()
@@ -127,68 +185,43 @@ class TorchComm:
         return torch.device("cpu")
 
     def all_gather(self, obj):
+        """Small host objects (driver utility; the protocol uses tensors)."""
         out = [None] * self.size
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
-    def alltoall(self, sends: dict):
-        """Blocks are tuples of tensors with identical structure on every rank
-        (same count, dtypes and trailing shapes); leading dims may differ."""
+    def all_gather_t(self, x):
+        import torch
+        x = x.to(self.device).contiguous()
+        out = torch.empty((self.size,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.all_gather_into_tensor(out, x, group=self.group)
+        else:
+            self.dist.all_gather(list(out.unbind(0)), x, group=self.group)
+        return out
+
+    def all_reduce_t(self, x):
+        x = x.to(self.device).contiguous().clone()
+        self.dist.all_reduce(x, group=self.group)
+        return x
+
+    def alltoallv(self, rows, send_counts):
         import torch
         dev = self.device
-        # describe every block so receivers know split sizes and shapes
-        meta = {d: [(tuple(t.shape), str(t.dtype)) for t in p] for d, p in sends.items()}
-        all_meta = self.all_gather(meta)
-        template = next((p for p in sends.values()), None)
-        if template is None:
-            for m in all_meta:
-                for v in m.values():
-                    template = v
-                    break
-                if template is not None:
-                    break
-        if template is None:
-            return {}
-        nfields = len(template)
-        got = {}
-        recv_shapes = {src: all_meta[src].get(self.rank) for src in range(self.size)}
-        for f in range(nfields):
-            send_parts, send_splits, recv_splits = [], [], []
-            dtype = None
-            for d in range(self.size):
-                if d in sends:
-                    t = sends[d][f].to(dev).contiguous()
-                    dtype = t.dtype
-                    send_parts.append(t.reshape(-1))
-                    send_splits.append(t.numel())
-                else:
-                    send_splits.append(0)
-            for src in range(self.size):
-                shp = recv_shapes[src]
-                if shp is None:
-                    recv_splits.append(0)
-                else:
-                    n = 1
-                    for s in shp[f][0]:
-                        n *= s
-                    recv_splits.append(n)
-                    dtype = dtype or getattr(torch, shp[f][1].replace("torch.", ""))
-            if dtype is None:
-                continue
-            send = torch.cat(send_parts) if send_parts else torch.empty(0, dtype=dtype, device=dev)
-            recv = torch.empty(sum(recv_splits), dtype=dtype, device=dev)
-            self.dist.all_to_all_single(recv, send, recv_splits, send_splits, group=self.group)
-            self.bytes_moved += int(sum(send_splits) - (send_splits[self.rank] if self.rank < len(send_splits) else 0)) \
-                * send.element_size()
-            off = 0
-            for src in range(self.size):
-                shp = recv_shapes[src]
-                if shp is None:
-                    continue
-                n = recv_splits[src]
-                got.setdefault(src, [None] * nfields)[f] = recv[off:off + n].reshape(shp[f][0])
-                off += n
-        return {s: tuple(v) for s, v in got.items()}
+        p = self.size
+        rows = rows.to(dev).contiguous()
+        sc_t = (send_counts.to(dev, torch.int64) if hasattr(send_counts, "to")
+                else torch.tensor(list(send_counts), dtype=torch.int64, device=dev)).contiguous()
+        rc_t = torch.empty(p, dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(rc_t, sc_t, group=self.group)
+        both = torch.cat([sc_t, rc_t]).tolist()  # the one host read of the exchange
+        sc, rc = both[:p], both[p:]
+        w = rows.shape[1] if rows.dim() == 2 else 1
+        out = torch.empty((sum(rc), w), dtype=rows.dtype, device=dev)
+        self.dist.all_to_all_single(out.view(-1), rows.view(-1), [c * w for c in rc], [c * w for c in sc],
+                                    group=self.group)
+        self.bytes_moved += (sum(sc) - sc[self.rank]) * w * rows.element_size()
+        return (out if rows.dim() == 2 else out.view(-1)), rc
 
     def barrier(self):
         self.dist.barrier(group=self.group)
@@ -200,7 +233,10 @@ def run_ranks(rank_count: int, program: Callable, args_per_rank: Sequence[tuple]
     cluster = ThreadCluster(rank_count)
 
     def body(r):
+        import torch
         try:
+            if torch.cuda.is_available():
+                torch.cuda.set_device(r % torch.cuda.device_count())
             return program(ThreadComm(cluster, r), *args_per_rank[r])
         except BaseException:
             cluster.abort()

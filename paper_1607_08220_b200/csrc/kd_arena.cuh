@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "kd_common.cuh"
@@ -62,5 +64,46 @@ struct ArenaScope {  // the calling thread's scratch comes from `a` while in sco
     }
 };
 
+
+// An arena bound to a (device, stream): calls that enqueue asynchronous work take their
+// temporaries from it; the next call on the same stream reuses it in stream order (the
+// earlier kernels finish before the later ones start), so no allocation and no sync.
+struct StreamArena {
+    std::unique_lock<std::mutex> lk;
+    Arena* prev;
+    StreamArena(int dev, cudaStream_t s) {
+        static std::mutex mu;
+        static std::map<std::pair<int, cudaStream_t>, std::pair<Arena*, std::mutex*>> by_stream;
+        std::pair<Arena*, std::mutex*> e;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            auto it = by_stream.find({dev, s});
+            if (it == by_stream.end()) {
+                Arena* a = new Arena();
+                a->device = dev;
+                it = by_stream.emplace(std::make_pair(dev, s), std::make_pair(a, new std::mutex())).first;
+            }
+            e = it->second;
+        }
+        lk = std::unique_lock<std::mutex>(*e.second);  // one host thread enqueues on a stream at a time
+        e.first->reset();
+        prev = t_arena;
+        t_arena = e.first;
+    }
+    ~StreamArena() { t_arena = prev; }
+    StreamArena(const StreamArena&) = delete;
+    StreamArena& operator=(const StreamArena&) = delete;
+};
+
+template <typename X>
+inline X* scratch(size_t count, cudaStream_t st) {
+    if (t_arena) return static_cast<X*>(t_arena->alloc(std::max<size_t>(count, 1) * sizeof(X)));
+    void* p = nullptr;
+    KD_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(X), st));
+    return static_cast<X*>(p);
+}
+inline void scratch_free(void* p, cudaStream_t st) {
+    if (p && !(t_arena && t_arena->owns(p))) cudaFreeAsync(p, st);
+}
 
 }  // namespace kdb

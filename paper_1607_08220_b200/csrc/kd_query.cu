@@ -31,16 +31,6 @@
 
 namespace kdb {
 
-template <typename X>
-static X* scratch(size_t count, cudaStream_t st) {
-    if (t_arena) return static_cast<X*>(t_arena->alloc(std::max<size_t>(count, 1) * sizeof(X)));
-    void* p = nullptr;
-    KD_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(X), st));
-    return static_cast<X*>(p);
-}
-static void scratch_free(void* p, cudaStream_t st) {
-    if (p && !(t_arena && t_arena->owns(p))) cudaFreeAsync(p, st);
-}
 
 constexpr int QCAP = 40;  // traversal stack capacity (tree depth + 2)
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
@@ -126,7 +116,8 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
 #pragma unroll
             for (int d = 0; d < DC; d++)
                 if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
-            if (admissible(fb) && sp < QCAP) {
+            if (admissible(fb)) {
+                if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
                 st_node[sp] = far;
 #pragma unroll
                 for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
@@ -440,7 +431,8 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 fo[d] = (d == dim) ? ad : off[d];
                 if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
             }
-            if (!first && admissible(fb) && sp < QCAP) {
+            if (!first && admissible(fb)) {
+                if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
                 st_node[sp] = far;
 #pragma unroll
                 for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
@@ -640,9 +632,10 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                 const int far = goleft ? rec.a : node + 1;
                 const float ad = __double2float_rz(fabs(qd - rec.v));
                 const float of = lane == dim ? ad : off;
-                if (admissible(bound_of(lane < D ? of : 0.0f)) && sp < QCAP) {
+                if (admissible(bound_of(lane < D ? of : 0.0f))) {
+                    if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
                     s_off[warp][sp][lane] = of;
-                    if (lane == 0) s_node[warp][sp] = far;
+                    s_node[warp][sp] = far;  // every lane stores the (warp-uniform) index: no cross-lane race
                     sp++;
                 }
                 node = near;
@@ -959,32 +952,8 @@ static bool knn_morton_order() {
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
     if (a.nq == 0) return;
-    // temporaries (sort keys, CUB scratch, work counters) from an arena bound to the stream:
-    // the next call on the same stream reuses it in stream order (no allocation, no sync)
-    struct KnnArena {
-        std::unique_lock<std::mutex> lk;
-        Arena* prev;
-        KnnArena(int dev, cudaStream_t s) {
-            static std::mutex mu;
-            static std::map<std::pair<int, cudaStream_t>, std::pair<Arena*, std::mutex*>> by_stream;
-            std::pair<Arena*, std::mutex*> e;
-            {
-                std::lock_guard<std::mutex> g(mu);
-                auto it = by_stream.find({dev, s});
-                if (it == by_stream.end()) {
-                    Arena* a = new Arena();
-                    a->device = dev;
-                    it = by_stream.emplace(std::make_pair(dev, s), std::make_pair(a, new std::mutex())).first;
-                }
-                e = it->second;
-            }
-            lk = std::unique_lock<std::mutex>(*e.second);  // one host thread enqueues on a stream at a time
-            e.first->reset();
-            prev = t_arena;
-            t_arena = e.first;
-        }
-        ~KnnArena() { t_arena = prev; }
-    } ka(t.device, st);
+    // temporaries (sort keys, CUB scratch, work counters) from the stream's arena
+    StreamArena ka(t.device, st);
     int32_t* order = nullptr;
     void* tmp = nullptr;
     uint32_t *k0 = nullptr, *k1 = nullptr;

@@ -85,11 +85,28 @@ def find_knn_device(tree: LocalTree, queries, k: int, radii=None, exclude_ids=No
     """Device-tensor variant: queries (nq, dims) float64 CUDA tensor.  Returns
     torch tensors (dists, ids(int64 view of uint64), counts, counters|None)."""
     import torch
+    if k < 1:
+        raise ValueError("k must be >= 1")
     if queries.dim() != 2 or queries.dtype != torch.float64 or not queries.is_cuda:
         raise ValueError("queries must be an (nq, dims) float64 CUDA tensor")
     queries = queries.contiguous()
     nq = queries.shape[0]
     dev = queries.device
+    if tree.count and queries.shape[1] != tree.dims:
+        raise ValueError(f"query dims {queries.shape[1]} != tree dims {tree.dims}")
+    tdev = tree.native(dev.index or 0).info().device
+    if (dev.index or 0) != tdev:
+        raise ValueError(f"queries are on cuda:{dev.index or 0} but the tree lives on cuda:{tdev}")
+
+    def _per_query(t, name, dtypes):
+        if t is None:
+            return None
+        if t.shape != (nq,) or t.dtype not in dtypes or t.device != dev:
+            raise ValueError(f"{name} must be an ({nq},) {'/'.join(str(d) for d in dtypes)} tensor on {dev}")
+        return t.contiguous()
+
+    radii = _per_query(radii, "radii", (torch.float64,))
+    exclude_ids = _per_query(exclude_ids, "exclude_ids", (torch.int64, torch.uint64))
     if out is None:
         od = torch.empty((nq, k), dtype=torch.float64, device=dev)
         oi = torch.empty((nq, k), dtype=torch.int64, device=dev)

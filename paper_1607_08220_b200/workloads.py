@@ -10,6 +10,16 @@ array would take longer to make than to index).
   C2  clustered 3D        N=64,000,000  Q=16,000,000 dataset rows k=5  leaf 32 (self excluded)
   C3  anisotropic sheet   N=256,000,000 Q=64,000,000 same law     k=5  leaf 32
   C4  10-D Gaussian mix   N=16,000,000  Q=4,000,000 same law      k=10 leaf 64
+  C5  clustered 3D, 65,536 halos, N=2,000,000,000 over 8 GPUs (250M per GPU shard),
+      Q=500,000,000 fresh draws (62.5M per shard), k=5, leaf 32, int64 ids >= 2^32
+
+Multi-GPU runs generate per-shard data on each GPU (``make_shard``): the halo
+catalogue (centres, widths, weights) is drawn once from a fixed seed, the points
+of shard s from seed(s) -- torch's CUDA generator is counter-based (Philox), so
+every GPU draws its own shard without a host array.  C3 keeps its stated total
+N at any GPU count (8 fixed shards assigned to ranks: strong scaling); C5 is one
+250M-point shard per GPU (weak scaling, 2B points at 8 GPUs) whose ids are
+(shard << 32) | row -- all above 2^32 but shard 0's.
 """
 
 from __future__ import annotations
@@ -34,24 +44,38 @@ CONFIGS = {
     "C2": Workload("C2-clustered3d", 64_000_000, 16_000_000, 3, 5, 32, True),
     "C3": Workload("C3-plasma3d", 256_000_000, 64_000_000, 3, 5, 32, False),
     "C4": Workload("C4-gauss10d", 16_000_000, 4_000_000, 10, 10, 64, False),
+    "C5": Workload("C5-clustered3d-2B", 2_000_000_000, 500_000_000, 3, 5, 32, False),
 }
+C5_SHARDS = 8          # BASELINE configs[4]: 8 GPUs
+C3_SHARDS = 8          # fixed partition of C3's 256M points / 64M queries for strong scaling
 
 
-def _halo_rows(torch, n, nh, g, dev):
+def _halo_catalogue(torch, nh, g, dev):
     centres = torch.rand((nh, 3), generator=g, device=dev, dtype=torch.float64)
     lo, hi = math.log(1e-3), math.log(1e-2)
     sig = torch.exp(torch.rand(nh, generator=g, device=dev, dtype=torch.float64) * (hi - lo) + lo)
     u = 1.0 - torch.rand(nh, generator=g, device=dev, dtype=torch.float64)  # (0, 1]
     w = u.pow(-1.0 / 1.5)  # Pareto(alpha=1.5, x_m=1) == numpy pareto(1.5) + 1
+    return centres, sig, w
+
+
+def _halo_rows(torch, n, nh, g, dev, catalogue=None):
+    centres, sig, w = catalogue if catalogue is not None else _halo_catalogue(torch, nh, g, dev)
     n_bg = n // 5
     n_h = n - n_bg
-    h = torch.multinomial(w, n_h, replacement=True, generator=g)
-    pts = centres[h] + torch.randn((n_h, 3), generator=g, device=dev, dtype=torch.float64) * sig[h, None]
-    del h
-    bg = torch.rand((n_bg, 3), generator=g, device=dev, dtype=torch.float64)
-    rows = torch.cat([pts, bg]).remainder_(1.0).to(torch.float32)
-    rows[rows >= 1.0] = 0.0  # periodic box: an f32 value rounded up to 1.0 wraps to 0
-    return rows
+    out = torch.empty((n, 3), device=dev, dtype=torch.float32)
+    step = 1 << 26  # bounded f64 temporaries for the 250M-point shards
+    for s in range(0, n_h, step):
+        e = min(n_h, s + step)
+        h = torch.multinomial(w, e - s, replacement=True, generator=g)
+        pts = centres[h] + torch.randn((e - s, 3), generator=g, device=dev, dtype=torch.float64) * sig[h, None]
+        out[s:e] = pts.remainder_(1.0).to(torch.float32)
+        del h, pts
+    for s in range(n_h, n, step):
+        e = min(n, s + step)
+        out[s:e] = torch.rand((e - s, 3), generator=g, device=dev, dtype=torch.float64).to(torch.float32)
+    out[out >= 1.0] = 0.0  # periodic box: an f32 value rounded up to 1.0 wraps to 0
+    return out
 
 
 def _sheet_rows(torch, n, g, dev):
@@ -97,7 +121,41 @@ def make_points(cfg: str, device="cuda", seed: int = 1000, n: int | None = None)
         return _sheet_rows(torch, n, g, device)
     if cfg == "C4":
         return _gauss10_rows(torch, n, g, device)
+    if cfg == "C5":  # one shard of the 65,536-halo law (the CPU baseline's bounded sample)
+        return make_shard("C5", 0, device, n=n, q=1)[0]
     raise ValueError(cfg)
+
+
+def make_shard(cfg: str, shard: int, device="cuda", n: int | None = None, q: int | None = None):
+    """(points (n, 3) float32, ids (n,) int64, queries (q, 3) float64) of one shard.
+    C5: 250M points / 62.5M queries per shard, 65,536-halo catalogue shared by all
+    shards, ids (shard << 32) | row.  C3: 1/8 of its 256M points / 64M queries."""
+    import torch
+    w = CONFIGS[cfg]
+    if cfg == "C5":
+        n = w.n // C5_SHARDS if n is None else n
+        q = w.q // C5_SHARDS if q is None else q
+        gc = torch.Generator(device=device)
+        gc.manual_seed(5005)
+        cat = _halo_catalogue(torch, 65536, gc, device)
+        g = torch.Generator(device=device)
+        g.manual_seed(6000 + shard)
+        pts = _halo_rows(torch, n, 65536, g, device, cat)
+        g.manual_seed(7000 + shard)
+        qs = _halo_rows(torch, q, 65536, g, device, cat).to(torch.float64)
+        ids = torch.arange(n, dtype=torch.int64, device=device) + (shard << 32)
+        return pts, ids, qs
+    if cfg == "C3":
+        n = w.n // C3_SHARDS if n is None else n
+        q = w.q // C3_SHARDS if q is None else q
+        g = torch.Generator(device=device)
+        g.manual_seed(1100 + shard)
+        pts = _sheet_rows(torch, n, g, device)
+        g.manual_seed(2100 + shard)
+        qs = _sheet_rows(torch, q, g, device).to(torch.float64)
+        ids = torch.arange(n, dtype=torch.int64, device=device) + shard * n
+        return pts, ids, qs
+    raise ValueError(f"{cfg}: sharded generation is defined for C3 and C5")
 
 
 def make_queries(cfg: str, rows, device="cuda", seed: int = 2000, q: int | None = None):

@@ -1,4 +1,4 @@
-"""Global tier on the GPU (CudaBackend): kd_histogram / kd_partition / device local
+"""Global tier on the GPU (CudaBackend): kd_histogram / kd_split_rows / device local
 builds / device KNN behind the SPMD protocol.  Bundles must equal the real
 reference's byte for byte; neighbours must equal the brute-force oracle;
 forwarding counters must equal the reference's (they depend only on r')."""
@@ -70,12 +70,13 @@ def test_unsplittable_raises():
 
 @pytest.mark.parametrize("p", [1, 2, 4, 8])
 def test_device_resident_protocol(p, oracle):
-    """dist_device.rank_query_device over in-process ranks (device tensors through
-    the communicator), global tier built with the device kernels."""
+    """dist_query.rank_query over in-process ranks (device tensors through the
+    communicator, kd_merge_topk on the owner), global tier built with the device
+    kernels, self-exclusion ids travelling with queries and requests."""
     import torch
-    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, rank_build_global
+    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, DeviceRegions, rank_build_global
     from paper_1607_08220_b200.comm import run_ranks
-    from paper_1607_08220_b200.dist_device import DeviceRegions, rank_query_device
+    from paper_1607_08220_b200.dist_query import QueryStats, rank_query
     from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
     rows = make_rows(60000, 3, 23, "halo-f32")
     n = rows.shape[0]
@@ -92,8 +93,8 @@ def test_device_resident_protocol(p, oracle):
         mine = qsel[qsel % p == comm.rank]
         q = torch.as_tensor(rows[mine]).to(dev)
         ex = torch.as_tensor(mine.astype(np.int64)).to(dev)
-        st = {}
-        d, i, cnt = rank_query_device(comm, tree, DeviceRegions(gt, dev), ex, q, k, excl=ex, stats=st)
+        st = QueryStats(rank=comm.rank)
+        d, i, r, cnt = rank_query(comm, tree, DeviceRegions(gt, dev), q, k, excl=ex, slice_size=700, stats=st)
         return mine, d.cpu().numpy(), i.cpu().numpy(), cnt.cpu().numpy(), st
 
     outs = run_ranks(p, prog, [() for _ in range(p)])
@@ -106,3 +107,72 @@ def test_device_resident_protocol(p, oracle):
             assert np.array_equal(d[r], bd[r, :bc[r]][keep][:k])
             assert np.array_equal(i[r].view(np.uint64), bi[r, :bc[r]][keep][:k])
         assert (cnt == k).all()
+        assert st.soundness_violations == 0
+
+
+def test_query_arrays_equals_objects(oracle):
+    from paper_1607_08220_b200.core import PointSet
+    from paper_1607_08220_b200.engine import RunConfig, build_engine
+    rows = make_rows(30000, 3, 8, "halo-f32")
+    ps = PointSet.from_rows(rows)
+    eng, _ = build_engine(ps, RunConfig(ranks=4, seed=2))
+    q = rows[::97] + 1e-5
+    (d, i, r, c), rep = eng.query_arrays(q, k=6)
+    res, _ = eng.query(q, k=6)
+    bd, bi, bc = oracle.brute_knn(ps.coords, ps.ids, q, 6)
+    assert np.array_equal(c, bc) and np.array_equal(d, bd) and np.array_equal(i, bi)
+    for j, rr in enumerate(res):
+        assert [x.point_id for x in rr.neighbors] == i[j, :c[j]].tolist()
+        assert [x.rank for x in rr.neighbors] == r[j, :c[j]].tolist()
+    # neighbour ranks: the rank whose region holds the point
+    owners = eng.ranks[0].global_tree.owner_of_batch(ps.coords.T[i[c > 0][:, 0].astype(np.int64)])
+    assert np.array_equal(owners, r[c > 0][:, 0])
+
+
+def test_c5_shards_int64_ids_three_levels_gpu(oracle):
+    """BASELINE configs[4] in miniature on the GPU: 8 thread ranks (3 global levels),
+    one C5-law shard each (ids (shard << 32) | row), the device protocol end to end."""
+    import torch
+    from paper_1607_08220_b200.cluster import ClusterConfig, DevicePoints, DeviceRegions, rank_build_global
+    from paper_1607_08220_b200.comm import run_ranks
+    from paper_1607_08220_b200.dist_query import QueryStats, rank_query
+    from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
+    from paper_1607_08220_b200.workloads import make_shard
+    p, n, nq, k = 8, 200_000, 2000, 5
+
+    def prog(comm):
+        pts, ids, q = make_shard("C5", comm.rank, comm.device, n=n, q=nq)
+        gt, mine, _ = rank_build_global(comm, DevicePoints(pts.t().contiguous(), ids), ClusterConfig(seed=4))
+        tree = build_local_tree_device(mine.coords, mine.ids, BuildConfig(seed=4))
+        st = QueryStats(rank=comm.rank)
+        d, i, r, c = rank_query(comm, tree, DeviceRegions(gt, comm.device), q, k, slice_size=4096, stats=st)
+        return (pts.cpu(), ids.cpu(), q.cpu().numpy(), d.cpu().numpy(), i.cpu().numpy().view(np.uint64),
+                c.cpu().numpy(), st)
+
+    outs = run_ranks(p, prog, [() for _ in range(p)])
+    coords = np.ascontiguousarray(torch.cat([o[0] for o in outs]).t().double().numpy())
+    ids = torch.cat([o[1] for o in outs]).numpy().view(np.uint64)
+    for _, _, q, d, i, c, st in outs:
+        sel = np.arange(0, q.shape[0], 7)
+        bd, bi, bc = oracle.brute_knn(coords, ids, q[sel], k)
+        assert np.array_equal(c[sel], bc) and np.array_equal(d[sel], bd) and np.array_equal(i[sel], bi)
+        assert st.soundness_violations == 0
+    assert sum(o[6].queries_forwarded for o in outs) > 0
+
+
+@pytest.mark.parametrize("name", ["u3_2000", "f32_u3_20000", "aniso3_5000"])
+def test_packet_kernel_matches_brute_force(name, oracle):
+    """The opt-in warp-per-packet kernel (KD_KNN_PACKET) gives the oracle's answers."""
+    from datagen import golden_cases
+    from paper_1607_08220_b200 import _native as N
+    from paper_1607_08220_b200 import core, local_query as lq, local_tree as lt
+    case = golden_cases()[name]
+    ps = core.PointSet.create(case["coords"], case["ids"])
+    tree = lt.build_local_tree(ps, lt.BuildConfig(**case["cfg"]))
+    for k in (1, 5, 8):
+        d, i, c, _ = lq.find_knn_batch(tree, case["queries"], k, flags=N.KD_KNN_PACKET)
+        bd, bi, bc = oracle.brute_knn(ps.coords, ps.ids, case["queries"], k)
+        m = np.arange(k)[None, :] < c[:, None]
+        assert np.array_equal(c, bc)
+        assert np.array_equal(np.where(m, d, 0), np.where(m, bd, 0)) and np.array_equal(np.where(m, i, 0),
+                                                                                          np.where(m, bi, 0))
