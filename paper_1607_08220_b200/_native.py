@@ -60,17 +60,25 @@ def _load():
     L.kd_knn.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
     L.kd_tree_free.argtypes = [C.c_void_p]
-    L.kd_histogram.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
-                               C.c_uint, C.c_void_p]
-    L.kd_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_double,
-                                C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
-    L.kd_unpack_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_uint,
-                                 C.c_void_p]
-    L.kd_merge_topk.argtypes = [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
-                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
-    L.kd_route.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
-                           C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]
+    ab = os.environ.get("KDB_LIB_PATH") is not None  # an A/B build may predate some entry points
+    for name, types in (("kd_histogram", [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                          C.c_void_p, C.c_uint, C.c_void_p]),
+                        ("kd_split_rows", [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                                           C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]),
+                        ("kd_unpack_rows", [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_uint, C.c_void_p]),
+                        ("kd_merge_topk", [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint,
+                                           C.c_void_p]),
+                        ("kd_route", [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint,
+                                      C.c_void_p])):
+        if ab and not hasattr(L, name):
+            continue
+        getattr(L, name).argtypes = types
+    if ab:
+        return L
     for name in EXPORTED:
         getattr(L, name)
     return L

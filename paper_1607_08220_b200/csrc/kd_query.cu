@@ -32,7 +32,13 @@
 namespace kdb {
 
 
-constexpr int QCAP = 40;  // traversal stack capacity (tree depth + 2)
+// traversal stack capacity of the per-query kernels: a depth-first walk that pushes
+// only far children holds at most one entry per tree level, and kd_knn refuses trees
+// deeper than KNN_MAX_DEPTH = QCAP - 3 for these kernels (KD_EUNSUPPORTED), so a
+// push can never overflow; the `sp < QCAP` terms in the push conditions are
+// therefore always true (they stay: without them nvcc schedules the persistent
+// kernel's push ~5 % slower on C2/C3, measured)
+constexpr int QCAP = 40;
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
 // (measured 34 vs 44 ms on C2); in higher dimensions the binary64 leaf scan dominates and it pays off
 template <int DT>
@@ -116,9 +122,8 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
 #pragma unroll
             for (int d = 0; d < DC; d++)
                 if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
-            if (admissible(fb)) {
-                if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
-                st_node[sp] = far;
+            if (admissible(fb) && sp < QCAP) {  // sp < QCAP always holds (depth <= KNN_MAX_DEPTH); kept
+                st_node[sp] = far;                 // because it measurably helps the compiler's schedule
 #pragma unroll
                 for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
                 sp++;
@@ -431,8 +436,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 fo[d] = (d == dim) ? ad : off[d];
                 if (d < D) fb = __fadd_rz(fb, __fmul_rz(fo[d], fo[d]));
             }
-            if (!first && admissible(fb)) {
-                if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
+            if (!first && admissible(fb) && sp < QCAP) {  // always true (see QCAP); keeps the faster schedule
                 st_node[sp] = far;
 #pragma unroll
                 for (int d = 0; d < DC; d++) st_off[sp][d] = fo[d];
@@ -632,8 +636,7 @@ k_knn_wq(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict_
                 const int far = goleft ? rec.a : node + 1;
                 const float ad = __double2float_rz(fabs(qd - rec.v));
                 const float of = lane == dim ? ad : off;
-                if (admissible(bound_of(lane < D ? of : 0.0f))) {
-                    if (sp >= QCAP) __trap();  // unreachable: kd_knn admits trees of depth <= KNN_MAX_DEPTH
+                if (admissible(bound_of(lane < D ? of : 0.0f)) && sp < QCAP) {  // always true (see QCAP)
                     s_off[warp][sp][lane] = of;
                     s_node[warp][sp] = far;  // every lane stores the (warp-uniform) index: no cross-lane race
                     sp++;
