@@ -176,3 +176,40 @@ def test_packet_kernel_matches_brute_force(name, oracle):
         assert np.array_equal(c, bc)
         assert np.array_equal(np.where(m, d, 0), np.where(m, bd, 0)) and np.array_equal(np.where(m, i, 0),
                                                                                           np.where(m, bi, 0))
+
+
+def _nccl_world1_worker(port, outq):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    try:
+        from paper_1607_08220_b200.comm import TorchComm, pack_rows, unpack_rows
+        c = TorchComm()
+        x = torch.arange(6, dtype=torch.int64, device=dev).reshape(2, 3)
+        g = c.all_gather_t(x)
+        r = c.all_reduce_t(x)
+        q = torch.rand((5, 3), dtype=torch.float64, device=dev)
+        rows, spec = pack_rows(torch.arange(5, device=dev), q, torch.arange(5, dtype=torch.int32, device=dev))
+        got, rc = c.alltoallv(rows, torch.tensor([5], device=dev))
+        a, b, cc = unpack_rows(got, spec)
+        empty, rc0 = c.alltoallv(rows[:0], [0])
+        outq.put((g.shape == (1, 2, 3) and torch.equal(g[0], x), torch.equal(r, x), rc == [5] and rc0 == [0],
+                  torch.equal(b, q) and torch.equal(a, torch.arange(5, device=dev)), empty.shape[0] == 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_nccl_collectives_world1():
+    """The NCCL code paths of TorchComm (all_gather_into_tensor, all_reduce,
+    all_to_all_single with split lists, packed rows) on CUDA tensors."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(29700 + os.getpid() % 200, q))
+    p.start()
+    res = q.get(timeout=180)
+    p.join(timeout=60)
+    assert p.exitcode == 0 and all(res), res
