@@ -81,7 +81,7 @@ def load_pkd1_device(path, device="cuda", chunk: int = 1 << 24):
         for s in range(0, count, chunk):
             e = min(count, s + chunk)
             torch.cuda.current_stream(out.device).synchronize()  # the staging buffer is free again
-            stage[:e - s].copy_(torch.from_numpy(np.asarray(cols[d, s:e])))
+            stage[:e - s].copy_(torch.from_numpy(np.array(cols[d, s:e])))
             out[d, s:e].copy_(stage[:e - s], non_blocking=True)
     dev_ids = torch.from_numpy(np.array(ids, dtype=np.uint64).view(np.int64)).to(device)
     if torch.unique(dev_ids).shape[0] != count:
