@@ -530,8 +530,34 @@ static __global__ void k_tile_info(const LNode* __restrict__ nodes, int K, int32
     tinfo[t] = TileInfo{ni, (int32_t)max((int64_t)0, e1 - e0), (int64_t)split[ni].dim * N + nd.start + e0};
 }
 
+// 1-D bulk copies (TMA engine, cp.async.bulk) into shared memory, completion counted
+// in bytes on an mbarrier -- one instruction per tile instead of one cp.async per element
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    if (bytes)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                     : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n KD_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra KD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// a tile's split-column values as one 16-byte-aligned span (the TMA's unit): the copy
+// starts at the aligned address below the first value; `lead` values precede it
+template <typename T>
+constexpr int HIST_SLOT = TILE + 32 / (int)sizeof(T);  // elements per tile buffer (alignment slack)
+
 // Persistent: each CTA streams a contiguous run of tiles; the next tile's values
-// are copied into the other shared buffer (cp.async) while the current one is
+// arrive by bulk copy into the other shared buffer while the current one is
 // classified, and the node's window / accumulators are only reloaded / flushed
 // when the run crosses into another node.
 template <typename T>
@@ -542,25 +568,34 @@ k_hist(const T* __restrict__ src, const TileInfo* __restrict__ tinfo, uint32_t t
     constexpr int HPT = EPT / SUB;  // elements per thread in each half-tile
     constexpr int NW = TILE_THREADS / 32;
     extern __shared__ __align__(16) unsigned char hist_dyn[];  // 2 tile buffers (dynamic: 64 KB for f64)
-    T (*buf)[TILE] = reinterpret_cast<T (*)[TILE]>(hist_dyn);
+    T (*buf)[HIST_SLOT<T>] = reinterpret_cast<T (*)[HIST_SLOT<T>]>(hist_dyn);
     __shared__ T sb[WIN];
     __shared__ uint32_t sf[SUB][WIN];
     __shared__ uint32_t nacc[WIN];
     __shared__ T q[NW][64];  // per-warp queue of in-window values (keeps the searches warp-dense)
     __shared__ uint32_t sL[SUB];
     __shared__ unsigned long long nL;
+    __shared__ __align__(8) uint64_t mbar[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t t0 = (uint32_t)((uint64_t)tiles * blockIdx.x / gridDim.x);
     const uint32_t t1 = (uint32_t)((uint64_t)tiles * (blockIdx.x + 1) / gridDim.x);
     if (t0 >= t1) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0]);
+        mbar_init(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto lead_of = [&](const TileInfo& ti) {
+        return (int)(((uintptr_t)(src + ti.off) & 15) / sizeof(T));
+    };
     auto issue = [&](const TileInfo& ti, int slot) {
-        const T* g = src + ti.off;
-#pragma unroll
-        for (int j = 0; j < EPT; j++) {
-            const int e = j * TILE_THREADS + threadIdx.x;
-            if (e < ti.cnt) cp_async_elem(&buf[slot][e], g + e);
+        if (threadIdx.x == 0) {
+            const char* g = reinterpret_cast<const char*>(src + ti.off);
+            const char* a = reinterpret_cast<const char*>((uintptr_t)g & ~(uintptr_t)15);
+            const unsigned bytes = ti.cnt ? (unsigned)(((g + (size_t)ti.cnt * sizeof(T) - a) + 15) & ~(size_t)15) : 0u;
+            bulk_load(buf[slot], a, bytes, &mbar[slot]);
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     TileInfo cur = tinfo[t0];
     issue(cur, 0);
@@ -570,7 +605,6 @@ k_hist(const T* __restrict__ src, const TileInfo* __restrict__ tinfo, uint32_t t
     for (uint32_t t = t0, it = 0; t < t1; t++, it++) {
         const int slot = it & 1;
         if (t + 1 < t1) issue(nxt, slot ^ 1);
-        else asm volatile("cp.async.commit_group;\n" ::: "memory");
         const TileInfo after = t + 2 < t1 ? tinfo[t + 2] : TileInfo{-1, 0, 0};
         if (cur.ni != cur_ni) {
             if (cur_ni >= 0) {  // flush the finished node
@@ -596,9 +630,9 @@ k_hist(const T* __restrict__ src, const TileInfo* __restrict__ tinfo, uint32_t t
             sf[1][i] = 0;
         }
         if (threadIdx.x < SUB) sL[threadIdx.x] = 0;
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
-        const T* tb = buf[slot];
+        mbar_wait(&mbar[slot], (it >> 1) & 1);  // this tile's bytes have landed
+        const T* tb = buf[slot] + lead_of(cur);
 #pragma unroll
         for (int h = 0; h < SUB; h++) {
             uint32_t* hist = sf[h];
@@ -1961,8 +1995,9 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         KD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, out->device));
         KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scatter<T, 3, 8>, TILE_THREADS, 0));
         scatter_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
-        KD_CUDA(cudaFuncSetAttribute(k_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * TILE * sizeof(T))));
-        KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hist<T>, TILE_THREADS, 2 * TILE * sizeof(T)));
+        KD_CUDA(cudaFuncSetAttribute(k_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * HIST_SLOT<T> * sizeof(T))));
+        KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hist<T>, TILE_THREADS, 2 * HIST_SLOT<T> * sizeof(T)));
         hist_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
     }
     int par = 0;  // buffer holding the current level's points
@@ -2028,7 +2063,7 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
             }
         }
         k_tile_info<<<(tiles + 255) / 256, 256, 0, st>>>(lv, K, tmap, split, tiles, c.N, tinfo);
-        k_hist<T><<<std::min<uint32_t>(tiles, hist_grid), TILE_THREADS, 2 * TILE * sizeof(T), st>>>(lsrc, tinfo, tiles, split, wb, wf, hrow,
+        k_hist<T><<<std::min<uint32_t>(tiles, hist_grid), TILE_THREADS, 2 * HIST_SLOT<T> * sizeof(T), st>>>(lsrc, tinfo, tiles, split, wb, wf, hrow,
                                                                                   hL);
         k_select<T><<<(K + 3) / 4, 128, 0, st>>>(lv, K, split, wb, wf, slow_list, slow_count);
         k_slow<T><<<std::min(K, 1024), SLOW_THREADS, 0, st>>>(lsrc, lv, c, split, slow_list, slow_count);
