@@ -415,7 +415,7 @@ def run_b200(args):
         ach_q = q * qb / tq / 1e9
         # build: 10 per breadth-first level (sample, tile info, hist, select, slow, tile-left, 2 scan,
         # scatter, children) + 2 per level preorder stitch + subtree, relocate, ids;
-        # query: 3-D Morton keys (box + keys), 6 CUB radix-sort kernels (32-bit keys), KNN (ncu list: 204 on C2)
+        # query: 3-D Morton keys (box + keys), CUB radix-sort kernels (32-bit keys), KNN (ncu list: 228 on C3)
         launches = 12 * levels + 3 + (9 if w.dims == 3 else 7)
         traffic = measured_traffic(args.config)
         line = {
@@ -437,13 +437,15 @@ def run_b200(args):
             "knn": {"value": world * q / tq, "unit": "queries/s",
                     "roofline": {"bound": "hbm", "achieved": ach_q, "peak": peak, "unit": "GB/s",
                                  "frac": ach_q / peak, "traffic": traffic.get("query_dram_bytes"),
-                                 "kernel": "query batch (home-leaf sort + k_knn_persist)",
+                                 "kernel": ("query batch (Morton sort + k_knn_persist)" if w.dims <= 3
+                                            else "query batch (home-leaf sort + k_knn_wq)"),
                                  "bytes_per_query": qb, "model": "4D+8V+4DC+16k", "V": v_ref, "C": c_ref,
                                  "counters": ctr_src}},
             "sample_check_vs_fp64_bruteforce": {"queries": min(16, q), "equal": ok},
             "sample_check_vs_reference_traversal": ref_check,
             "build_levels": levels,
             "build_slow_nodes": slow_nodes,
+            "build_phases_ms": {k: tree.build_info[k] for k in ("ms_levels", "ms_subtree", "ms_finish")},
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
