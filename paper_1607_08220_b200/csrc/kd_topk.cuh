@@ -25,8 +25,8 @@ __device__ __forceinline__ bool lexless_pos(double d0, uint32_t p0, double d1, u
 // has checked that it enters): one descending pass, each slot keeps, shifts from
 // its predecessor, or takes the new entry; ids are read only on exact ties
 template <int KM>
-__device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
-                                                uint32_t p, const uint64_t* __restrict__ ids) {
+__device__ __forceinline__ void topk_insert_pos_tie(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
+                                                    uint32_t p, const uint64_t* __restrict__ ids) {
     const int last = cnt < k ? cnt : k - 1;
     bool placed = false;
 #pragma unroll
@@ -42,6 +42,35 @@ __device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)
                 bp[jj] = p;
                 placed = true;
             }
+        }
+    }
+    if (cnt < k) cnt++;
+}
+
+// Slots at or beyond the fill count hold +inf (the kernels initialise the list so),
+// so without an exact distance tie each slot j either keeps its entry (it is below d),
+// takes d (its predecessor is below d, it is not), or takes its predecessor: one
+// comparison per slot and selects, no branches.  A tie with a listed distance (rare)
+// takes the id-ordered path above.
+template <int KM>
+__device__ __forceinline__ void topk_insert_pos(double (&bd)[KM], uint32_t (&bp)[KM], int& cnt, int k, double d,
+                                                uint32_t p, const uint64_t* __restrict__ ids) {
+    bool tie = false;
+#pragma unroll
+    for (int j = 0; j < KM; j++) tie |= bd[j] == d;
+    if (tie) {
+        topk_insert_pos_tie<KM>(bd, bp, cnt, k, d, p, ids);
+        return;
+    }
+    bool below[KM];
+#pragma unroll
+    for (int j = 0; j < KM; j++) below[j] = bd[j] < d;
+#pragma unroll
+    for (int j = KM - 1; j >= 0; j--) {
+        if (j < k && !below[j]) {
+            const bool here = j == 0 || below[j > 0 ? j - 1 : 0];
+            bd[j] = here ? d : bd[j > 0 ? j - 1 : 0];
+            bp[j] = here ? p : bp[j > 0 ? j - 1 : 0];
         }
     }
     if (cnt < k) cnt++;
