@@ -291,7 +291,10 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     const bool has_ex = excl != nullptr;
     // with an excluded id the search keeps k+1 candidates and drops that id at
     // output: top-(k+1) minus {ex}, truncated to k == top-k of the set minus {ex}
-    const int kk = k + (has_ex ? 1 : 0);
+    // the dispatcher picks KM == k(+1) exactly for 1, 2, 5, 6: then the list length is a
+    // compile-time constant (the insertion's slot guards and the k-th-slot pick fold away)
+    constexpr bool EXACT = KM == 1 || KM == 2 || KM == 5 || KM == 6;
+    const int kk = EXACT ? KM : k + (has_ex ? 1 : 0);
     int64_t qi = -1;
     int64_t c0 = 0, c1 = 0, c2 = 0;
     double bd[KM];
