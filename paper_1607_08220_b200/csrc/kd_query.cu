@@ -263,6 +263,80 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
 }
 
 // ----------------------------------------------------------------------------
+// Home pass of the two-pass 2-D/3-D search: one thread per query in sorted order
+// descends to the query's home leaf (no stack) and keeps the kk smallest binary64
+// distances of that bucket (values only, branch-free min/max chain).  The kk-th
+// one is an upper bound on the query's final kk-th distance: k_knn_persist starts
+// from it, so its traversal prunes from the first node and only the few points
+// inside the bound reach the list insertion.  Every lane of a warp is in the same
+// phase here, which the persistent kernel (lanes at arbitrary points of their
+// walks) cannot offer to the insertion-heavy first bucket.
+// bound0[t] = +inf when the bucket holds fewer than kk points with d < radius.
+// ----------------------------------------------------------------------------
+template <typename T, int DT, int KM>
+__global__ void __launch_bounds__(128)
+k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords, int64_t n,
+           const double* __restrict__ queries, const int32_t* __restrict__ order, int64_t nq, int kk,
+           const double* __restrict__ radii, double* __restrict__ bound0) {
+    static_assert(DT > 0, "fixed-dimension instances only");
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nq) return;
+    const int64_t qi = order ? (int64_t)order[t] : t;
+    double q[DT];
+#pragma unroll
+    for (int d = 0; d < DT; d++) q[d] = queries[qi * DT + d];
+    const double radius = radii ? radii[qi] : INFINITY;
+    if (n_nodes <= 0) { bound0[t] = INFINITY; return; }
+    int node = 0;
+    KdNode rec = nodes[0];
+    while (rec.db >= 0) {
+        double qd = q[0];
+#pragma unroll
+        for (int d = 1; d < DT; d++)
+            if (d == rec.db) qd = q[d];
+        node = qd < rec.v ? node + 1 : rec.a;
+        rec = nodes[node];
+    }
+    const int start = rec.a, end = rec.a + (-1 - rec.db);
+    double bd[KM];
+#pragma unroll
+    for (int j = 0; j < KM; j++) bd[j] = INFINITY;
+    constexpr int UN = 4;
+    for (int base = start; base < end; base += UN) {
+        T cv[UN][DT];
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+            const int i = min(base + u, end - 1);
+#pragma unroll
+            for (int d = 0; d < DT; d++) cv[u][d] = coords[(int64_t)d * n + i];
+        }
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+            double dist = 0.0;
+#pragma unroll
+            for (int d = 0; d < DT; d++) {
+                const double df = __dsub_rn((double)cv[u][d], q[d]);
+                dist = __dadd_rn(dist, __dmul_rn(df, df));
+            }
+            // a repeated point (the clamped tail) or one outside the radius does not enter
+            double x = (base + u < end && dist < radius) ? dist : INFINITY;
+#pragma unroll
+            for (int j = 0; j < KM; j++) {
+                const bool lt = x < bd[j];
+                const double lo = lt ? x : bd[j];
+                x = lt ? bd[j] : x;
+                bd[j] = lo;
+            }
+        }
+    }
+    double b = bd[KM - 1];
+#pragma unroll
+    for (int j = 0; j < KM - 1; j++)
+        if (j == kk - 1) b = bd[j];
+    bound0[t] = b;
+}
+
+// ----------------------------------------------------------------------------
 // Persistent warps with dynamic query fetch.  Each lane runs its own exact
 // traversal (same bounds / admission rules as k_knn); when a lane finishes its
 // query it takes the next one from a warp-local pool of leaf-sorted queries,
@@ -271,14 +345,18 @@ k_knn(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ c
 // slowest query) while keeping neighbouring lanes on neighbouring queries.
 // ----------------------------------------------------------------------------
 // low-dimensional, small-k instances are held to 72 registers (7 CTAs of 4 warps per SM)
-template <typename T, int DT, int KM>
+// SCAN: 0 = the lane walks its own push-free first descent and inserts inline while scanning;
+//       2 = two-pass: the k-th distance bound comes from k_knn_home (bound0, by sorted position),
+//           and buckets are scanned in chunks whose hits are inserted afterwards (see below)
+template <typename T, int DT, int KM, int SCAN = 0>
 __global__ void __launch_bounds__(128, (DT > 0 && DT <= 3 && KM <= 8) ? 7 : 1)
 k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
               const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
               const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
               const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
               int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter,
-              bool push_free_first, const uint32_t* __restrict__ home_keys) {
+              bool push_free_first, const uint32_t* __restrict__ home_keys,
+              const double* __restrict__ bound0 = nullptr) {
     constexpr int DC = Dims<DT>::cap;
     constexpr int POOL = 64;
     const int D = DT > 0 ? DT : dims_rt;
@@ -313,8 +391,12 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
     int pool_left = 0;
     bool exhausted = false;
 
+    // admission threshold kth_d: the radius (strict) until the list is full or a bound from the
+    // home pass is known, then a distance that kk points are known to reach (inclusive)
+    bool strict = true;
     auto admissible = [&](float b) {
         const double bb = (double)b;
+        if constexpr (SCAN == 2) return strict ? bb < kth_d : bb <= kth_d;
         return cnt < kk ? bb < radius : bb <= kth_d;
     };
     // exact fp32 pre-filter for float trees: a point whose binary64 distance d
@@ -392,7 +474,12 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 }
                 sp = 0;
                 home = -1;
-                first = push_free_first;
+                first = SCAN == 2 ? false : push_free_first;
+                if constexpr (SCAN == 2) {
+                    const double t0 = bound0[myq];
+                    strict = !(t0 < INFINITY);
+                    if (!strict) kth_d = t0;  // < radius: the home pass admits d < radius only
+                }
 #pragma unroll
                 for (int d = 0; d < DC; d++) off[d] = 0.0f;
                 // -2: finished immediately (empty tree).  With the home-leaf sort keys the
@@ -452,6 +539,51 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
             const int start = lstart, len = llen;
             c1++;
             c2 += len;
+            if constexpr (SCAN == 2) {
+                // Chunked scan with deferred insertion.  A chunk's binary64 distances stay in
+                // registers; each is compared with the threshold as it stands (a superset test:
+                // the threshold only tightens) and the hits are recorded in a bit mask, then
+                // drained one per iteration.  With 32 independent lanes some lane hits at almost
+                // every point, so inline insertion runs its ~80 instructions on nearly every step
+                // for a handful of lanes; here it runs max-over-lanes(hits per chunk) times.
+                constexpr int CH = 4;
+                const int end = start + len;
+                for (int base = start; base < end; base += CH) {
+                    double dv[CH];
+                    unsigned cand = 0;
+#pragma unroll
+                    for (int u = 0; u < CH; u++) {
+                        const int i = min(base + u, end - 1);
+                        double dist = 0.0;
+#pragma unroll
+                        for (int d = 0; d < DC; d++) {
+                            if (d < D) {
+                                const double df = __dsub_rn((double)coords[(int64_t)d * n + i], q[d]);
+                                dist = __dadd_rn(dist, __dmul_rn(df, df));
+                            }
+                        }
+                        dv[u] = dist;
+                        cand |= (unsigned)(dist <= kth_d && base + u < end) << u;
+                    }
+                    while (cand) {
+                        const int u = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        double dist = dv[0];
+#pragma unroll
+                        for (int v = 1; v < CH; v++)
+                            if (u == v) dist = dv[v];
+                        const int i = base + u;
+                        if (cnt < kk ? (strict ? dist < kth_d : dist <= kth_d)
+                                     : (dist <= kth_d && lexless_pos(dist, (uint32_t)i, kth_d, kth_p, ids))) {
+                            topk_insert_pos<KM>(bd, bp, cnt, kk, dist, (uint32_t)i, ids);
+                            if (cnt == kk) {
+                                topk_last<KM>(bd, bp, kk, kth_d, kth_p);
+                                strict = false;
+                            }
+                        }
+                    }
+                }
+            } else {
             // software pipeline: the next point's coordinates are in flight while this one is
             // evaluated (the binary64 conversion no longer waits on the load; -9 % on C2/C3)
             T nx[DC];
@@ -497,6 +629,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                         }
                     }
                 }
+            }
             }
         }
         // ---- after the home leaf: restart from the root with a real k-th distance
@@ -820,6 +953,16 @@ static bool knn_push_free_first() {
     return v;
 }
 
+// 2-D/3-D search with k(+1) <= 8: 2 = two-pass (k_knn_home + deferred-insertion scan, default),
+// 0 = single persistent kernel with inline insertion (KDB_KNN_SCAN, for A/B measurements)
+static int knn_scan_mode() {
+    static const int v = [] {
+        const char* e = getenv("KDB_KNN_SCAN");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
 template <typename T, int DT, int KM>
 static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, const uint32_t* home,
                        cudaStream_t st) {
@@ -857,6 +1000,22 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
             unsigned long long* ctr = scratch<unsigned long long>(1, st);
             KD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+            if constexpr (DT > 0 && DT <= 3 && KM <= 8) {
+                if (knn_scan_mode() == 2) {
+                    double* bound0 = scratch<double>((size_t)a.nq, st);
+                    const int kk = (int)a.k + (a.excl ? 1 : 0);
+                    k_knn_home<T, DT, KM><<<(unsigned)((a.nq + 127) / 128), 128, 0, st>>>(
+                        t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.n, a.queries, order, a.nq, kk,
+                        a.radii, bound0);
+                    k_knn_persist<T, DT, KM, 2><<<grid, threads, 0, st>>>(
+                        t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order,
+                        a.nq, (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, false, nullptr,
+                        bound0);
+                    scratch_free(bound0, st);
+                    scratch_free(ctr, st);
+                    return;
+                }
+            }
             k_knn_persist<T, DT, KM><<<grid, threads, 0, st>>>(
                 t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order, a.nq,
                 (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, knn_push_free_first(), home);
