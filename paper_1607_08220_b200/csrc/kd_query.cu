@@ -277,7 +277,7 @@ template <typename T, int DT, int KM>
 __global__ void __launch_bounds__(128)
 k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords, int64_t n,
            const double* __restrict__ queries, const int32_t* __restrict__ order, int64_t nq, int kk,
-           const double* __restrict__ radii, double* __restrict__ bound0) {
+           const double* __restrict__ radii, double* __restrict__ bound0, int32_t* __restrict__ entry) {
     static_assert(DT > 0, "fixed-dimension instances only");
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nq) return;
@@ -286,7 +286,7 @@ k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restric
 #pragma unroll
     for (int d = 0; d < DT; d++) q[d] = queries[qi * DT + d];
     const double radius = radii ? radii[qi] : INFINITY;
-    if (n_nodes <= 0) { bound0[t] = INFINITY; return; }
+    if (n_nodes <= 0) { bound0[t] = INFINITY; entry[t] = 0; return; }
     int node = 0;
     KdNode rec = nodes[0];
     while (rec.db >= 0) {
@@ -334,6 +334,27 @@ k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restric
     for (int j = 0; j < KM - 1; j++)
         if (j == kk - 1) b = bd[j];
     bound0[t] = b;
+    // Entry node: on the root-to-home path the query lies on the near side of every plane
+    // (all box offsets zero), and a far child whose bound |q - v|^2 exceeds the bound b can
+    // never be admitted (the threshold only tightens).  The walk may therefore start at the
+    // first node of the path whose far child is admissible -- same bound arithmetic and the
+    // same test as k_knn_persist's push -- instead of the root.
+    int e = 0;
+    if (b < INFINITY) {
+        rec = nodes[0];
+        while (rec.db >= 0) {
+            double qd = q[0];
+#pragma unroll
+            for (int d = 1; d < DT; d++)
+                if (d == rec.db) qd = q[d];
+            const float ad = __double2float_rz(fabs(qd - rec.v));
+            const float fb = __fadd_rz(0.0f, __fmul_rz(ad, ad));
+            if ((double)fb <= b) break;
+            e = qd < rec.v ? e + 1 : rec.a;
+            rec = nodes[e];
+        }
+    }
+    entry[t] = e;
 }
 
 // ----------------------------------------------------------------------------
@@ -356,7 +377,7 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
               const uint64_t* __restrict__ excl, double* __restrict__ out_d, uint64_t* __restrict__ out_i,
               int64_t* __restrict__ out_c, int64_t* __restrict__ out_ctr, unsigned long long* __restrict__ counter,
               bool push_free_first, const uint32_t* __restrict__ home_keys,
-              const double* __restrict__ bound0 = nullptr) {
+              const double* __restrict__ bound0 = nullptr, const int32_t* __restrict__ entry = nullptr) {
     constexpr int DC = Dims<DT>::cap;
     constexpr int POOL = 64;
     const int D = DT > 0 ? DT : dims_rt;
@@ -485,6 +506,9 @@ k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __rest
                 // -2: finished immediately (empty tree).  With the home-leaf sort keys the
                 // first (push-free) descent is a jump: k_leaf_of already walked it.
                 node = n_nodes > 0 ? ((home_keys && first) ? (int)home_keys[myq] : 0) : -2;
+                if constexpr (SCAN == 2) {
+                    if (n_nodes > 0) node = entry[myq];
+                }
             }
         }
         if (node == -2) {
@@ -1003,14 +1027,16 @@ static void launch_knn(const KdTreeDev& t, const KnnArgs& a, const int32_t* orde
             if constexpr (DT > 0 && DT <= 3 && KM <= 8) {
                 if (knn_scan_mode() == 2) {
                     double* bound0 = scratch<double>((size_t)a.nq, st);
+                    int32_t* entry = scratch<int32_t>((size_t)a.nq, st);
                     const int kk = (int)a.k + (a.excl ? 1 : 0);
                     k_knn_home<T, DT, KM><<<(unsigned)((a.nq + 127) / 128), 128, 0, st>>>(
                         t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.n, a.queries, order, a.nq, kk,
-                        a.radii, bound0);
+                        a.radii, bound0, entry);
                     k_knn_persist<T, DT, KM, 2><<<grid, threads, 0, st>>>(
                         t.nodes, t.n_nodes, static_cast<const T*>(t.coords), t.ids, t.n, t.dims, a.queries, order,
                         a.nq, (int)a.k, a.radii, a.excl, a.out_d, a.out_i, a.out_c, a.out_ctr, ctr, false, nullptr,
-                        bound0);
+                        bound0, entry);
+                    scratch_free(entry, st);
                     scratch_free(bound0, st);
                     scratch_free(ctr, st);
                     return;
