@@ -1192,14 +1192,15 @@ struct SubStack {
     uint32_t packed;     // start (10 bits) | n (11 bits) << 10 | rel depth (11 bits) << 21
 };
 
-constexpr int FY_SLOTS = 8192;  // global scratch slots for the rare exact-variance path
+constexpr int FY_SLOTS = 8192;
+constexpr int SUB_WARPS_HOST = 2;  // == SUB_WARPS (k_subtree)  // global scratch slots for the rare exact-variance path
 
 __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
     size_t b = (size_t)dims * ts * tsize;
     b = (b + 15) & ~size_t(15);
     b += (size_t)2 * ts * 2;  // perm ping-pong by depth parity
     b = (b + 15) & ~size_t(15);
-    b += 256 * 4;             // radix histogram
+    b += SUB_WARPS_HOST * 256 * 4;  // radix histogram per warp
     return b;
 }
 
@@ -1298,7 +1299,7 @@ template <typename T>
 __device__ __noinline__ int sub_exact_dim(const T* cs, const uint16_t* pm, int n, int ts, int D, unsigned ncmask,
                                           uint64_t path, const DevCtx& c, uint32_t* fyslots, int* fylocks) {
     const int lane = threadIdx.x & 31;
-    const int slot = blockIdx.x % FY_SLOTS;
+    const int slot = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % FY_SLOTS;
     if (lane == 0) while (atomicCAS(&fylocks[slot], 0, 1) != 0) {}
     __syncwarp();
     __threadfence();
@@ -1561,17 +1562,31 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
 }
 
 
+// Two warps per task (SUB_WARPS): warp 0 splits the task's root, then the warps
+// build the two child subtrees concurrently (disjoint ranges of the shared
+// permutation, own radix histogram, own node / stack regions: a subtree of m
+// points has at most 2m-1 nodes, so the right subtree is numbered from 0 at
+// offset 2*nl and moved down behind the left one at the end).  Same shared
+// memory per task as one warp, twice the resident warps per SM.
+constexpr int SUB_WARPS = 2;
+constexpr int SUB_THREADS = SUB_WARPS * 32;
+
+__device__ __forceinline__ void pair_sync() {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(SUB_THREADS) : "memory");
+}
+
 template <typename T, int DT>
-__global__ void __launch_bounds__(32, 13)
+__global__ void __launch_bounds__(SUB_THREADS, 12)
 k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, int32_t* idx0, const int32_t* idx1, DevCtx c,
           KdNode* __restrict__ scratch, int32_t* __restrict__ scnt, SubStack* __restrict__ sstack,
           uint32_t* __restrict__ fyslots, int* __restrict__ fylocks, int32_t* task_nodes, int32_t* task_depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Task tk = tasks[blockIdx.x];
+    const int task = blockIdx.x;
+    const Task tk = tasks[task];
     const int D = DT > 0 ? DT : c.dims;
     const int64_t N = c.N;
     const int ts = c.ts;
-    const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // tk.src: 0 / 1 = build buffer, 2 = the caller's input (row ids = positions)
     const T* src = tk.src == 2 ? in0 : (tk.src ? buf1 : buf0);
     const int32_t* isrc = tk.src == 2 ? nullptr : (tk.src ? idx1 : idx0);
@@ -1582,16 +1597,16 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
     if (tk.leaf || tk.n > ts) {
         // degenerate leaf (possibly larger than the shared-memory limit): copy through
         if (tk.src) {
-            for (int64_t e = lane; e < tk.n; e += 32) {
+            for (int64_t e = tid; e < tk.n; e += SUB_THREADS) {
                 for (int d = 0; d < D; d++) buf0[(int64_t)d * N + tk.start + e] = src[(int64_t)d * N + tk.start + e];
                 idx0[tk.start + e] = isrc ? isrc[tk.start + e] : (int32_t)(tk.start + e);
             }
         }
-        if (lane == 0) {
+        if (tid == 0) {
             out_nodes[0] = KdNode{0.0, (int32_t)tk.start, -1 - tk.n};
             out_cnt[0] = tk.n;
-            task_nodes[blockIdx.x] = 1;
-            task_depth[blockIdx.x] = tk.depth;
+            task_nodes[task] = 1;
+            task_depth[task] = tk.depth;
         }
         return;
     }
@@ -1603,15 +1618,18 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
     perm[0] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
     perm[1] = reinterpret_cast<uint16_t*>(p); p += (size_t)ts * 2;
     p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~uintptr_t(15));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    uint32_t* hist_all = reinterpret_cast<uint32_t*>(p);
+    uint32_t* hist = hist_all + warp * 256;
+    // warp 1's histogram doubles as the mailbox of the root hand-off (it is idle until then)
+    volatile int32_t* mbox = reinterpret_cast<volatile int32_t*>(hist_all + 256);
     // stage the task's points with asynchronous copies (all loads in flight at once)
-    for (int e = lane; e < n; e += 32) {
+    for (int e = tid; e < n; e += SUB_THREADS) {
         for (int d = 0; d < D; d++) cp_async_elem(&cs[d * ts + e], &src[(int64_t)d * N + tk.start + e]);
         perm[0][e] = (uint16_t)e;
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
+    pair_sync();
     auto emit = [&](const uint16_t* pm, int st, int len) {
         for (int e = lane; e < len; e += 32) {
             const int qv = pm[st + e];
@@ -1623,7 +1641,26 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
     int cursor = 0, maxd = 0, sp = 0;
     int st = 0, nn = n, rd = 0, parent_pre = -1;
     uint64_t path = tk.path;
-    for (;;) {
+    bool at_root = warp == 0;  // warp 0 is about to process the task's root
+    bool work = true;
+    int nl_root = 0;
+    if (warp != 0) {
+        pair_sync();  // root done
+        const int nl0 = mbox[0];
+        __syncwarp();
+        if (nl0 < 0) {
+            work = false;  // the root is a leaf
+        } else {
+            st = nl0;
+            nn = n - nl0;
+            rd = 1;
+            path = tk.path * 2ULL + 1ULL;
+            out_nodes += 2 * nl0;
+            out_cnt += 2 * nl0;
+            stk += 2 * nl0;
+        }
+    }
+    while (work) {
         const int pre = cursor++;
         if (parent_pre >= 0 && lane == 0) out_nodes[parent_pre].a = pre;  // right child index
         maxd = max(maxd, rd);
@@ -1632,9 +1669,16 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
         if (nn > c.bucket) {
             const uint16_t* pmn = ((rd & 1) ? perm[1] : perm[0]) + st;
             if constexpr (DT > 0) {
+#if defined(KD_SUB_NO_SMALL)
+                sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
+#elif defined(KD_SUB_NO_SMALL4)
+                if (nn <= 64) sub_split_small<T, DT, 2>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
+                else sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
+#else
                 if (nn <= 64) sub_split_small<T, DT, 2>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
                 else if (nn <= 128) sub_split_small<T, DT, 4>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
                 else sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
+#endif
             } else {
                 sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
             }
@@ -1645,6 +1689,11 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
                 out_cnt[pre] = nn;
             }
             emit(perm[rd & 1], st, nn);
+            if (at_root) {
+                if (lane == 0) mbox[0] = -1;
+                pair_sync();
+                at_root = false;
+            }
             if (sp == 0) break;
             sp--;
             const SubStack e = stk[sp];
@@ -1678,36 +1727,83 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
             }
         }
         __syncwarp();
-        if (lane == 0) {
-            out_nodes[pre] = KdNode{val, -1, dim};
-            out_cnt[pre] = nn;
-            stk[sp] = SubStack{path * 2ULL + 1ULL, pre,
-                               (uint32_t)(st + nl) | ((uint32_t)(nn - nl) << 10) | ((uint32_t)(rd + 1) << 21)};
+        if (at_root) {
+            // hand the right child to warp 1 (its index, the size of this warp's part, is patched in below)
+            if (lane == 0) {
+                out_nodes[pre] = KdNode{val, -1, dim};
+                out_cnt[pre] = nn;
+                mbox[0] = nl;
+            }
+            nl_root = nl;
+            pair_sync();
+            at_root = false;
+        } else {
+            if (lane == 0) {
+                out_nodes[pre] = KdNode{val, -1, dim};
+                out_cnt[pre] = nn;
+                stk[sp] = SubStack{path * 2ULL + 1ULL, pre,
+                                   (uint32_t)(st + nl) | ((uint32_t)(nn - nl) << 10) | ((uint32_t)(rd + 1) << 21)};
+            }
+            sp++;
         }
-        sp++;
         path = path * 2ULL;
         parent_pre = -1;
         nn = nl;
         rd = rd + 1;
         __syncwarp();
     }
-    // row ids in the final order; the source may alias the output, so read all before writing
+    // both parts done: move the right subtree's nodes down behind the left part
     __syncwarp();
-    int32_t rid[MAXS / 32];
+    if (!work) cursor = 0;
+    if (lane == 0) {
+        hist[0] = (uint32_t)cursor;
+        hist[1] = (uint32_t)maxd;
+        hist[2] = (uint32_t)nl_root;
+    }
+    pair_sync();
+    const int c0 = (int)hist_all[0], c1 = (int)hist_all[256];
+    const int md = max((int)hist_all[1], (int)hist_all[257]);
+    if (c1 > 0) {
+        // the right part was numbered from 0 at scratch index 2*nl (nl = the root's left count)
+        const int nl0 = (int)hist_all[2];
+        KdNode* base_nodes = scratch + 2 * tk.start;
+        int32_t* base_cnt = scnt + 2 * tk.start;
+        const KdNode* rs = base_nodes + 2 * nl0;
+        const int32_t* rc = base_cnt + 2 * nl0;
+        for (int b = 0; b < c1; b += SUB_THREADS) {  // destination <= source: ascending chunks, read before write
+            const int i = b + tid;
+            KdNode nd = KdNode{0.0, 0, 0};
+            int32_t cn = 0;
+            if (i < c1) {
+                nd = rs[i];
+                cn = rc[i];
+                if (nd.db >= 0) nd.a += c0;
+            }
+            pair_sync();
+            if (i < c1) {
+                base_nodes[c0 + i] = nd;
+                base_cnt[c0 + i] = cn;
+            }
+            pair_sync();
+        }
+        if (tid == 0) base_nodes[0].a = c0;
+    }
+    // row ids in the final order; the source may alias the output, so read all before writing
+    int32_t rid[MAXS / SUB_THREADS];
 #pragma unroll
-    for (int k2 = 0; k2 < MAXS / 32; k2++) {
-        const int e = k2 * 32 + lane;
+    for (int k2 = 0; k2 < MAXS / SUB_THREADS; k2++) {
+        const int e = k2 * SUB_THREADS + tid;
         if (e < n) rid[k2] = isrc ? isrc[tk.start + perm[0][e]] : (int32_t)(tk.start + perm[0][e]);
     }
-    __syncwarp();
+    pair_sync();
 #pragma unroll
-    for (int k2 = 0; k2 < MAXS / 32; k2++) {
-        const int e = k2 * 32 + lane;
+    for (int k2 = 0; k2 < MAXS / SUB_THREADS; k2++) {
+        const int e = k2 * SUB_THREADS + tid;
         if (e < n) idx0[tk.start + e] = rid[k2];
     }
-    if (lane == 0) {
-        task_nodes[blockIdx.x] = cursor;
-        task_depth[blockIdx.x] = tk.depth + maxd;
+    if (tid == 0) {
+        task_nodes[task] = c0 + c1;
+        task_depth[task] = tk.depth + md;
     }
 }
 
@@ -2128,11 +2224,11 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     int* fylocks = reinterpret_cast<int*>(fyslots + (size_t)FY_SLOTS * 2 * MAXS);
     if (dims == 3) {
         KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
-        k_subtree<T, 3><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
+        k_subtree<T, 3><<<ntasks, SUB_THREADS, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
                                                       fyslots, fylocks, task_nodes, task_depth);
     } else {
         KD_CUDA(cudaFuncSetAttribute(k_subtree<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
-        k_subtree<T, 0><<<ntasks, 32, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
+        k_subtree<T, 0><<<ntasks, SUB_THREADS, sub_smem, st>>>(tasks, buf[0], buf[1], d_in, idx[0], idx[1], c, scratch, scnt, sstack,
                                                       fyslots, fylocks, task_nodes, task_depth);
     }
     KD_CUDA(cudaGetLastError());
