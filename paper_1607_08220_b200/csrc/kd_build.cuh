@@ -140,6 +140,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const int take = (int)min((int64_t)n, c.vs);
     const uint64_t vseed = node_seed(c.seed, nd.path, 0);
     if (direct) fy_direct<32>(n, take, vseed, dlast, gidx, picked);
+    else if constexpr (!BIG) fy_hash<32>(n, take, vseed, reinterpret_cast<uint32_t*>(skeys), gidx, picked);
     else fy_resolve<32, FK>(n, take, vseed, skeys, picked, gidx);
 
     int d0 = 0;
@@ -214,6 +215,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
     const uint64_t mseed = node_seed(c.seed, nd.path, 1ULL + (uint64_t)d0);
     __syncwarp();
     if (direct) fy_direct<32>(n, m, mseed, dlast, gidx, picked);
+    else if constexpr (!BIG) fy_hash<32>(n, m, mseed, reinterpret_cast<uint32_t*>(skeys), gidx, picked);
     else fy_resolve<32, FK>(n, m, mseed, skeys, picked, gidx);
     typedef typename KeyOf<T>::type Key;
     const T* row = src + (int64_t)d0 * N + nd.start;

@@ -274,4 +274,92 @@ __device__ __noinline__ void fy_direct(uint32_t n, int m, uint64_t seed, uint16_
     __syncwarp();
 }
 
+// Partial Fisher-Yates for nodes of FYD_MAX < n <= 2^22 points: the algorithm of
+// fy_direct with the last[] table replaced by an open-addressing hash table of
+// FYH_SLOTS entries (target << 10 | latest step) -- at most m <= 1024 distinct
+// targets are ever recorded, so the table is at most half full and needs no
+// sorting of the draws (fy_resolve) whatever the node size.
+//   lookup  by the lowest lane of every same-target group of a 32-step round
+//           (the other lanes' previous step is the next lower lane of the group);
+//   insert  by the same lane, after every lookup of the round has finished:
+//           the group's highest step overwrites the target's entry, or claims
+//           the free slot that ended the probe (atomicCAS against other groups).
+// Shared scratch: tab[FYH_SLOTS] u32, back[m] u16, picked[m] u32.
+constexpr int FYH_SLOTS = 2048;
+constexpr uint32_t FYH_EMPTY = 0xFFFFFFFFu;
+constexpr uint32_t FYH_NONE = 1023u;  // a previous step is < 1023
+
+__device__ __forceinline__ uint32_t fyh_slot(uint32_t tgt) { return (tgt * 2654435761u) >> 21; }
+
+// entry of `tgt`: returns the step recorded for it (FYH_NONE if absent); h = its slot or the free slot that ended the probe
+__device__ __forceinline__ uint32_t fyh_find(const uint32_t* tab, uint32_t tgt, uint32_t& h) {
+    h = fyh_slot(tgt);
+    for (;;) {
+        const uint32_t e = tab[h];
+        if (e == FYH_EMPTY) return FYH_NONE;
+        if ((e >> 10) == tgt) return e & 1023u;
+        h = (h + 1) & (FYH_SLOTS - 1);
+    }
+}
+
+template <int R>
+__device__ __noinline__ void fy_hash(uint32_t n, int m, uint64_t seed, uint32_t* tab, uint16_t* back, uint32_t* picked) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    for (int i = lane; i < FYH_SLOTS; i += 32) tab[i] = FYH_EMPTY;
+    __syncwarp();
+#pragma unroll 1
+    for (int r = 0; r < R; r++) {
+        const int j = r * 32 + lane;
+        const bool act = j < m;
+        uint32_t tgt = 0xFFFFFFFFu;
+        if (act) {
+            const uint64_t z = rng_at(seed, (uint64_t)j);
+            tgt = (uint32_t)j + (uint32_t)mod_u64_u32(z, n - (uint32_t)j);
+        }
+        const unsigned grp = __match_any_sync(FULL, tgt);
+        const unsigned lower = grp & lt;
+        uint32_t pv = FYH_NONE, h = 0;
+        if (act) {
+            if (lower) pv = (uint32_t)(r * 32 + 31 - __clz(lower));
+            else pv = fyh_find(tab, tgt, h);
+        }
+        __syncwarp();
+        if (act && !lower) {
+            const uint32_t val = (tgt << 10) | (uint32_t)(r * 32 + 31 - __clz(grp));
+            if (pv != FYH_NONE) {
+                tab[h] = val;  // the target's own entry: no other group writes it
+            } else {
+                for (;;) {  // claim a free slot (other groups may race for the same one)
+                    const uint32_t old = atomicCAS(&tab[h], FYH_EMPTY, val);
+                    if (old == FYH_EMPTY) break;
+                    h = (h + 1) & (FYH_SLOTS - 1);
+                }
+            }
+        }
+        if (act) picked[j] = tgt | (pv << 22);
+        __syncwarp();
+    }
+    // back(t) = latest step i < t that targeted slot t: step t's own previous step if it
+    // targeted itself, else the final entry of t (no later step can target t)
+    for (int j = lane; j < m; j += 32) {
+        const uint32_t w = picked[j];
+        uint32_t h;
+        const uint32_t b = (w & 0x3FFFFFu) == (uint32_t)j ? (w >> 22) : fyh_find(tab, (uint32_t)j, h);
+        back[j] = (uint16_t)b;
+    }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) {
+        const uint32_t w = picked[j];
+        uint32_t i = w >> 22;
+        uint32_t val = w & 0x3FFFFFu;
+        if (i != FYH_NONE) {
+            while (back[i] != FYH_NONE) i = back[i];
+            val = i;
+        }
+        picked[j] = val;
+    }
+    __syncwarp();
+}
+
 }  // namespace kdb
