@@ -1120,6 +1120,145 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
     }
 }
 
+// k_scatter_tma: the same stable partition for points of few dimensions, fed by
+// the TMA engine.  A half-tile's D coordinate columns and its row ids arrive by
+// 1-D bulk copies (cp.async.bulk + mbarrier) into one of two shared-memory
+// stages; the next half-tile's copies are in flight while the current one is
+// classified, prefixed and written -- the read stream never waits for the
+// block-wide prefix or the stores (the register-staged k_scatter alternates
+// load and store phases and reaches 5.2 TB/s).
+template <typename T>
+constexpr int SCAT_SLOT = TILE / SUB + 32 / (int)sizeof(T);  // elements per column buffer (alignment slack)
+template <typename T, int DT>
+constexpr size_t scat_stage_bytes() {
+    return ((size_t)DT * SCAT_SLOT<T> * sizeof(T) + (size_t)SCAT_SLOT<int32_t> * sizeof(int32_t) + 15) & ~size_t(15);
+}
+
+template <typename T, int DT>
+__global__ void __launch_bounds__(TILE_THREADS)
+k_scatter_tma(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __restrict__ dst,
+              int32_t* __restrict__ idst, const HalfMeta* __restrict__ meta, DevCtx c,
+              const uint32_t* __restrict__ tile_loff, uint32_t nhalf) {
+    constexpr int NW = TILE_THREADS / 32;
+    constexpr int CH = TILE / SUB / TILE_THREADS;  // chunks of 256 elements per half-tile
+    constexpr int HS = SCAT_SLOT<T>;
+    extern __shared__ __align__(16) unsigned char scat_dyn[];
+    __shared__ uint32_t wl[CH * NW];
+    __shared__ uint32_t wpre[CH * NW];
+    __shared__ __align__(8) uint64_t mbar[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t N = c.N;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0]);
+        mbar_init(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto stage_cols = [&](int slot) { return reinterpret_cast<T*>(scat_dyn + (size_t)slot * scat_stage_bytes<T, DT>()); };
+    auto stage_ids = [&](int slot) { return reinterpret_cast<int32_t*>(stage_cols(slot) + (size_t)DT * HS); };
+    // one thread: expect the half-tile's bytes, then one bulk copy per column (+ ids)
+    auto issue = [&](uint32_t hb, int slot) {
+        const HalfMeta hm = meta[hb];
+        const int64_t cnt = (int64_t)hm.e1 - hm.e0;
+        unsigned bytes[DT + 1];
+        const char* from[DT + 1];
+        unsigned total = 0;
+#pragma unroll
+        for (int d = 0; d <= DT; d++) {
+            bytes[d] = 0;
+            from[d] = nullptr;
+            if (cnt <= 0 || (d == DT && !isrc)) continue;
+            const char* g = d < DT ? reinterpret_cast<const char*>(src + (int64_t)d * N + hm.gbase + hm.e0)
+                                   : reinterpret_cast<const char*>(isrc + hm.gbase + hm.e0);
+            const size_t esz = d < DT ? sizeof(T) : sizeof(int32_t);
+            const char* a = reinterpret_cast<const char*>((uintptr_t)g & ~(uintptr_t)15);
+            from[d] = a;
+            bytes[d] = (unsigned)(((g + (size_t)cnt * esz - a) + 15) & ~(size_t)15);
+            total += bytes[d];
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&mbar[slot])), "r"(total)
+                     : "memory");
+#pragma unroll
+        for (int d = 0; d <= DT; d++) {
+            if (!bytes[d]) continue;
+            void* to = d < DT ? (void*)(stage_cols(slot) + (size_t)d * HS) : (void*)stage_ids(slot);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                         ::"r"(smem_u32(to)), "l"(from[d]), "r"(bytes[d]), "r"(smem_u32(&mbar[slot]))
+                         : "memory");
+        }
+    };
+    if (threadIdx.x == 0 && blockIdx.x < nhalf) issue(blockIdx.x, 0);
+    uint32_t it = 0;
+    for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x, it++) {
+        const int slot = it & 1;
+        if (threadIdx.x == 0 && hb + gridDim.x < nhalf) issue(hb + gridDim.x, slot ^ 1);
+        const HalfMeta hm = meta[hb];
+        mbar_wait(&mbar[slot], (it >> 1) & 1);  // this half-tile's bytes have landed (0 bytes: at once)
+        if (hm.e1 > hm.e0) {
+            const int cnt = hm.e1 - hm.e0;
+            const int64_t gbase = hm.gbase;
+            const uint32_t lbefore = tile_loff[hb] - tile_loff[hm.first_hb];  // lefts earlier in this node
+            const int64_t lrun = lbefore;
+            const int64_t rrun = (int64_t)hm.e0 - lbefore;
+            const T* col[DT];
+#pragma unroll
+            for (int d = 0; d < DT; d++)
+                col[d] = stage_cols(slot) + (size_t)d * HS +
+                         (((uintptr_t)(src + (int64_t)d * N + gbase + hm.e0) & 15) / sizeof(T));
+            const int32_t* icol = stage_ids(slot) + (isrc ? ((uintptr_t)(isrc + gbase + hm.e0) & 15) / sizeof(int32_t) : 0);
+            const T* scol = col[0];
+#pragma unroll
+            for (int d = 1; d < DT; d++)
+                if (d == hm.dim) scol = col[d];
+            bool f[CH];
+            unsigned bal[CH];
+#pragma unroll
+            for (int j = 0; j < CH; j++) {
+                const int e = j * TILE_THREADS + threadIdx.x;
+                f[j] = e < cnt && (double)scol[e < cnt ? e : 0] < hm.value;
+                bal[j] = __ballot_sync(FULL, f[j]);
+                if (lane == 0) wl[j * NW + warp] = __popc(bal[j]);
+            }
+            __syncthreads();
+            if (warp == 0) {  // exclusive prefix over (chunk, warp) in element order
+                constexpr int PER = (CH * NW + 31) / 32;
+                uint32_t loc[PER], sum = 0;
+#pragma unroll
+                for (int q = 0; q < PER; q++) {
+                    const int i = lane * PER + q;
+                    loc[q] = sum;
+                    sum += i < CH * NW ? wl[i] : 0;
+                }
+                uint32_t incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const uint32_t ex = incl - sum;
+#pragma unroll
+                for (int q = 0; q < PER; q++) {
+                    const int i = lane * PER + q;
+                    if (i < CH * NW) wpre[i] = ex + loc[q];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < CH; j++) {
+                const int e = j * TILE_THREADS + threadIdx.x;
+                if (e >= cnt) continue;
+                const uint32_t lp = wpre[j * NW + warp] + __popc(bal[j] & ((1u << lane) - 1));
+                const int64_t pos = f[j] ? lrun + lp : hm.nl + rrun + ((int64_t)e - lp);
+                const int64_t gd = gbase + pos;
+#pragma unroll
+                for (int d = 0; d < DT; d++) dst[(int64_t)d * N + gd] = col[d][e];
+                idst[gd] = isrc ? icol[e] : (int32_t)(gbase + hm.e0 + e);  // level 0: ids = input rows
+            }
+        }
+        __syncthreads();  // the stage is free for the copy issued two iterations on; wl / wpre reusable
+    }
+}
+
 // ============================================================================
 // k_children: records + next level + subtree tasks
 // ============================================================================
@@ -2088,11 +2227,26 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
         return e ? atoi(e) : 1024;
     }();
     uint32_t scatter_grid = 0, hist_grid = 0;  // resident CTAs of the persistent scatter / histogram
+    uint32_t scatter_tma_grid = 0;
+    size_t scatter_tma_smem = 0;
+    static const bool scatter_tma = std::getenv("KDB_NO_SCATTER_TMA") == nullptr;
     {
         int sms = 148, per = 0;
         KD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, out->device));
         KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scatter<T, 3, 8>, TILE_THREADS, 0));
         scatter_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
+        if (dims == 2 || dims == 3) {  // TMA-fed variant: two shared-memory stages per CTA
+            const size_t sb = 2 * (dims == 2 ? scat_stage_bytes<T, 2>() : scat_stage_bytes<T, 3>());
+            if (dims == 2) {
+                KD_CUDA(cudaFuncSetAttribute(k_scatter_tma<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+                KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scatter_tma<T, 2>, TILE_THREADS, sb));
+            } else {
+                KD_CUDA(cudaFuncSetAttribute(k_scatter_tma<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+                KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scatter_tma<T, 3>, TILE_THREADS, sb));
+            }
+            scatter_tma_grid = (uint32_t)sms * (uint32_t)std::max(per, 1);
+            scatter_tma_smem = sb;
+        }
         KD_CUDA(cudaFuncSetAttribute(k_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * HIST_SLOT<T> * sizeof(T))));
         KD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_hist<T>, TILE_THREADS, 2 * HIST_SLOT<T> * sizeof(T)));
@@ -2180,14 +2334,18 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
 #define KD_SCATTER(DTV, CHV)                                                                                   \
     k_scatter<T, DTV, CHV><<<std::min<uint32_t>(tiles * SUB, scatter_grid), TILE_THREADS, 0, st>>>(                  \
         lsrc, lidx, buf[1 - par], idx[1 - par], hmeta, c, tile_loff, tiles * SUB)
+#define KD_SCATTER_TMA(DTV)                                                                                     \
+    k_scatter_tma<T, DTV><<<std::min<uint32_t>(tiles * SUB, scatter_tma_grid), TILE_THREADS, scatter_tma_smem, st>>>( \
+        lsrc, lidx, buf[1 - par], idx[1 - par], hmeta, c, tile_loff, tiles * SUB)
         switch (dims) {
             case 1: KD_SCATTER(1, 8); break;
-            case 2: KD_SCATTER(2, 8); break;
-            case 3: KD_SCATTER(3, 8); break;
+            case 2: if (scatter_tma) KD_SCATTER_TMA(2); else KD_SCATTER(2, 8); break;
+            case 3: if (scatter_tma) KD_SCATTER_TMA(3); else KD_SCATTER(3, 8); break;
             case 4: KD_SCATTER(4, 8); break;
             default: KD_SCATTER(0, 2); break;
         }
 #undef KD_SCATTER
+#undef KD_SCATTER_TMA
         LNode* next = dalloc<LNode>(2 * (size_t)K, st);
         k_children<<<(K + 255) / 256, 256, 0, st>>>(lv, K, split, c, 1 - par, at_input ? 2 : par, (int)ts_used, ts, next, next_ctr,
                                                     tasks, task_ctr, next_max);
