@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-build-sample", type=int, default=4_000_000)
     p.add_argument("--cpu-query-sample", type=int, default=200_000)
+    p.add_argument("--no-ref-counters", action="store_true", help="skip the device replay of the reference walk")
+    p.add_argument("--ref-counter-queries", type=int, default=4_000_000)
     return p.parse_args()
 
 
@@ -402,11 +404,34 @@ def run_b200(args):
         ref_check = reference_rows_check(cpu.pop("rows"), od[:nqs], oi[:nqs], oc[:nqs],
                                          None if excl is None else excl[:nqs], w.k)
 
+    # reference-definition counters on the device: KD_KNN_REFERENCE replays the reference's own
+    # walk (local_query.py:72-172) over this tree; V, C of the query model come from it (a larger
+    # sample than the host leg can afford) and are cross-checked against the oracle's on its sample
+    gpu_ctr = None
+    if rank == 0 and not args.no_ref_counters:
+        kk = w.k + (1 if w.queries_from_data else 0)
+        nref = min(q, args.ref_counter_queries if w.dims <= 3 else 20000)
+        _, _, _, ctr = find_knn_device(tree, queries[:nref], kk, counters=True, flags=N.KD_KNN_REFERENCE)
+        torch.cuda.synchronize()
+        gpu_ctr = {"queries": int(nref), "V": float(ctr[:, 0].double().mean()), "C": float(ctr[:, 2].double().mean()),
+                   "source": "KD_KNN_REFERENCE walk on the device (kd_walk.cu), reference definition"}
+        if cpu is not None:
+            m = min(nref, cpu["knn_sample_queries"])
+            gpu_ctr["equal_oracle_counters"] = bool(
+                abs(float(ctr[:m, 0].double().mean()) - cpu["ref_nodes_visited"]) < 1e-9 and
+                abs(float(ctr[:m, 2].double().mean()) - cpu["ref_points_compared"]) < 1e-9) \
+                if m == cpu["knn_sample_queries"] else None
+        del ctr
+
     if rank == 0:
         peak, peak_kind = peaks()
         bbytes, levels_model = build_bytes(n, w.dims, w.leaf)
         ach_b = bbytes / tb / 1e9
-        if cpu is not None:
+        if gpu_ctr is not None:
+            v_ref, c_ref = gpu_ctr["V"], gpu_ctr["C"]
+            ctr_src = (f"reference-definition counters from the device replay of the reference walk over the "
+                       f"full-size tree ({gpu_ctr['queries']} queries)")
+        elif cpu is not None:
             v_ref, c_ref = cpu["ref_nodes_visited"], cpu["ref_points_compared"]
             ctr_src = "reference counters (oracle traversal over the identical full-size tree, sample)"
         else:
@@ -443,7 +468,7 @@ def run_b200(args):
                                  "kernel": ("query batch (Morton sort + k_knn_persist)" if w.dims <= 3
                                             else "query batch (home-leaf sort + k_knn_wq)"),
                                  "bytes_per_query": qb, "model": "4D+8V+4DC+16k", "V": v_ref, "C": c_ref,
-                                 "counters": ctr_src}},
+                                 "counters": ctr_src, "gpu_reference_walk": gpu_ctr}},
             "sample_check_vs_fp64_bruteforce": {"queries": min(16, q), "equal": ok},
             "sample_check_vs_reference_traversal": ref_check,
             "build_levels": levels,

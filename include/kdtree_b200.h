@@ -57,6 +57,7 @@ extern "C" {
 #define KD_DEVICE_PTRS 1u     /* all array arguments are device pointers */
 #define KD_NO_SORT 2u         /* kd_knn: keep caller query order (no leaf sort) */
 #define KD_THREAD_PER_QUERY 4u /* kd_knn: one thread per query, no dynamic fetch (default: persistent warps) */
+#define KD_KNN_REFERENCE 16u  /* kd_knn: walk the tree exactly as local_query.py:72-172 (binary64 incremental bounds, prune at bound >= r'): results and counters bit-identical to the reference, tie quirk included */
 #define KD_KNN_PACKET 8u      /* kd_knn, D <= 3: one warp per 32-query packet over tight boxes (default: per-lane traversals) */
 
 typedef struct kd_tree kd_tree;

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("KDB_LIB_PATH") or os.path.join(_HERE, "libkdtree_b200
 
 KD_OK, KD_EINVAL, KD_ECUDA, KD_EUNSUPPORTED, KD_ENOMEM = 0, -1, -2, -3, -4
 KD_F32, KD_F64 = 1, 2
-KD_DEVICE_PTRS, KD_NO_SORT, KD_THREAD_PER_QUERY, KD_KNN_PACKET = 1, 2, 4, 8
+KD_DEVICE_PTRS, KD_NO_SORT, KD_THREAD_PER_QUERY, KD_KNN_PACKET, KD_KNN_REFERENCE = 1, 2, 4, 8, 16
 
 EXPORTED = ("kd_version", "kd_last_error", "kd_device_count", "kd_tree_build", "kd_tree_import",
             "kd_tree_get_info", "kd_tree_export", "kd_knn", "kd_tree_free", "kd_histogram", "kd_split_rows",

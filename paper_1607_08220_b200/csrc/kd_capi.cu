@@ -333,9 +333,10 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
     // per-query kernels carry a fixed stack
     const bool packet = (flags & KD_KNN_PACKET) && t->dev.dims <= 3 && k + (exclude_ids ? 1 : 0) <= 32 &&
                         !(flags & KD_THREAD_PER_QUERY);
-    if (!packet && t->dev.depth > KNN_MAX_DEPTH)
-        return fail(KD_EUNSUPPORTED, "tree deeper than the device traversal stack (" +
-                                         std::to_string(KNN_MAX_DEPTH) + ")");
+    const bool ref_walk = (flags & KD_KNN_REFERENCE) != 0;
+    if (ref_walk && exclude_ids) return fail(KD_EINVAL, "KD_KNN_REFERENCE: the reference walk has no id exclusion");
+    // trees deeper than the fast kernels' fixed stack take the depth-sized walk (kd_walk.cu)
+    const bool walk = ref_walk || (!packet && t->dev.depth > KNN_MAX_DEPTH);
     if (nq == 0) return KD_OK;
     KD_TRY({
         const KdTreeDev& d = t->dev;
@@ -349,13 +350,13 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         a.sort_queries = !(flags & KD_NO_SORT);
         a.thread_per_query = (flags & KD_THREAD_PER_QUERY) != 0;
         a.packet = (flags & KD_KNN_PACKET) != 0;
-        if (a.packet) {  // the packet kernel's query tree (tight boxes) is built on first use
+        if (a.packet && !walk) {  // the packet kernel's query tree (tight boxes) is built on first use
             std::lock_guard<std::mutex> lk(const_cast<kd_tree*>(t)->mu);
             if (!d.qnodes) build_qtree(const_cast<KdTreeDev*>(&d), st);
         }
         DevBuf bq, br, be, bd, bi, bc, bctr;
         DevBuf hd, hi;
-        if (k > 32 || (k == 32 && exclude_ids && !a.thread_per_query)) {  // heap kernel scratch
+        if (!walk && (k > 32 || (k == 32 && exclude_ids && !a.thread_per_query))) {  // heap kernel scratch
             new (&hd) DevBuf(nq * k * 8, st);
             new (&hi) DevBuf(nq * k * 8, st);
             a.heap_d = (double*)hd.p;
@@ -364,7 +365,8 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
         if (dev_ptrs) {
             a.queries = queries; a.radii = radii; a.excl = exclude_ids;
             a.out_d = out_d; a.out_i = out_i; a.out_c = out_c; a.out_ctr = out_ctr;
-            knn(d, a, st);
+            if (walk) knn_walk(d, a, ref_walk, st);
+            else knn(d, a, st);
             return KD_OK;
         }
         ArenaScope scope(d.device);  // synchronous below: staging from the arena
@@ -428,7 +430,8 @@ int kd_knn(const kd_tree* t, const double* queries, int64_t nq, int64_t k, const
             ac.out_c = (int64_t*)bc.p + lo;
             ac.out_ctr = out_ctr ? (int64_t*)bctr.p + lo * 3 : nullptr;
             if (a.heap_d) { ac.heap_d = a.heap_d + lo * k; ac.heap_i = a.heap_i + lo * k; }
-            knn(d, ac, st);
+            if (walk) knn_walk(d, ac, ref_walk, st);
+            else knn(d, ac, st);
             KD_CUDA(cudaEventRecord(evs[2 * c + 1], st));
             KD_CUDA(cudaStreamWaitEvent(s_out, evs[2 * c + 1], 0));
             KD_CUDA(cudaMemcpyAsync(out_d + lo * k, ac.out_d, cnt * k * 8, cudaMemcpyDeviceToHost, s_out));

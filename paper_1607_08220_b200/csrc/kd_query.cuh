@@ -29,6 +29,8 @@ constexpr int64_t KNN_CHUNK_MIN = 1 << 20;  // host-buffer pipeline: queries per
 constexpr int64_t KNN_MAX_CHUNKS = 8;
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st);
+// kd_walk.cu: any depth / any k; reference = true walks exactly as local_query.py:72-172 (results and counters)
+void knn_walk(const KdTreeDev& t, const KnnArgs& a, bool reference, cudaStream_t st);
 bool knn_packet(const KdTreeDev& t, const KnnArgs& a, const int32_t* order, cudaStream_t st);  // kd_packet.cu
 
 }  // namespace kdb

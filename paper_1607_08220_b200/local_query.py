@@ -21,13 +21,19 @@ __all__ = ["find_knn", "find_knn_batch", "count_visited", "find_knn_device"]
 
 
 def find_knn_batch(tree: LocalTree, queries, k: int, radii=np.inf, workers: int = 1, *,
-                   exclude_ids=None, counters: bool = True, device: int = 0, flags: int = 0):
+                   exclude_ids=None, counters: bool = True, device: int = 0, flags: int = 0,
+                   reference_walk: bool = False):
     """Exact KNN for a block of queries against one tree.
 
     Returns (dists (nq,k) f64, ids (nq,k) u64, counts (nq,) i64, counters (nq,3) i64);
     row i holds counts[i] valid entries sorted by (sq_dist, point_id).  ``radii``
     is a scalar or per-query array of squared radii (strict).  ``exclude_ids``
     (extension): one point id per query that is never returned (self-exclusion).
+    ``reference_walk`` (extension): traverse exactly as the reference does
+    (local_query.py:72-172: binary64 incremental bounds, pruning at bound >= r') --
+    results and counters are then bit-identical to the reference's, its tie quirk
+    included; the default walk has the brute-force oracle's tie semantics and counts
+    its own (shorter) traversal.
     """
     if k < 1:
         raise ValueError("k must be >= 1")
@@ -57,6 +63,8 @@ def find_knn_batch(tree: LocalTree, queries, k: int, radii=np.inf, workers: int 
         if ex.shape != (nq,):
             raise ValueError("exclude_ids must hold one id per query")
     nt = tree.native(device)
+    if reference_walk:
+        flags |= N.KD_KNN_REFERENCE
     N.check(N.lib.kd_knn(nt.handle, q.ctypes.data, nq, k, None if r is None else r.ctypes.data,
                          None if ex is None else ex.ctypes.data, out_d.ctypes.data, out_i.ctypes.data,
                          out_c.ctypes.data, out_ctr.ctypes.data if counters else None, flags, None))
@@ -73,9 +81,10 @@ def find_knn(tree: LocalTree, q, k: int, sq_radius: float = np.inf, query_id: in
 
 
 def count_visited(tree: LocalTree, q, k: int, sq_radius: float = np.inf) -> dict:
-    """Traversal counters for one query (local_query.py:229-237)."""
+    """Traversal counters for one query (local_query.py:229-237): the reference's own walk
+    is replayed on the device, so the counters equal the reference's."""
     q = np.asarray(q, dtype=np.float64).reshape(1, -1)
-    _, _, _, ctr = find_knn_batch(tree, q, k, sq_radius)
+    _, _, _, ctr = find_knn_batch(tree, q, k, sq_radius, reference_walk=True)
     return {"nodes_visited": int(ctr[0, 0]), "buckets_scanned": int(ctr[0, 1]),
             "points_compared": int(ctr[0, 2])}
 

@@ -98,6 +98,88 @@ def test_knn_on_imported_reference_tree(api, name):
         assert np.array_equal(mi, knn[f"{name}/k{k}/brute_ids"])
 
 
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_reference_walk_equals_reference_outputs_and_counters(api, name):
+    """KD_KNN_REFERENCE replays local_query.py:72-172 on the device: dists, ids, counts and
+    the (nodes visited, buckets scanned, points compared) counters equal what the real
+    reference returned for the same tree and queries (golden), tie quirk included."""
+    core, lt, lq = api
+    case = CASES[name]
+    knn = np.load(os.path.join(GOLD, "knn.npz"))
+    ps = core.PointSet.create(case["coords"], case["ids"])
+    tree = lt.build_local_tree(ps, lt.BuildConfig(**case["cfg"]))
+    for k in case["ks"]:
+        d, i, c, ctr = lq.find_knn_batch(tree, case["queries"], k, reference_walk=True)
+        assert np.array_equal(c, knn[f"{name}/k{k}/counts"])
+        md, mi = masked(d, i, c)
+        assert np.array_equal(md, knn[f"{name}/k{k}/dists"])
+        assert np.array_equal(mi, knn[f"{name}/k{k}/ids"])
+        assert np.array_equal(ctr, knn[f"{name}/k{k}/counters"])
+    if case.get("radius") is not None:
+        k = case["ks"][0]
+        d, i, c, _ = lq.find_knn_batch(tree, case["queries"], k, radii=case["radius"], reference_walk=True)
+        assert np.array_equal(c, knn[f"{name}/r/counts"])
+        md, mi = masked(d, i, c)
+        assert np.array_equal(md, knn[f"{name}/r/dists"]) and np.array_equal(mi, knn[f"{name}/r/ids"])
+
+
+def test_reference_walk_keeps_the_tie_quirk(api):
+    """the reference returns id 9 where the brute-force oracle returns id 3."""
+    core, lt, lq = api
+    case = CASES["q5_quirk"]
+    ps = core.PointSet.create(case["coords"], case["ids"])
+    tree = lt.build_local_tree(ps, lt.BuildConfig(**case["cfg"]))
+    _, i_ref, _, _ = lq.find_knn_batch(tree, case["queries"], 1, reference_walk=True)
+    _, i_def, _, _ = lq.find_knn_batch(tree, case["queries"], 1)
+    assert int(i_ref[0, 0]) == 9 and int(i_def[0, 0]) == 3
+
+
+def test_count_visited_equals_reference_counters(api):
+    core, lt, lq = api
+    case = CASES["u3_2000"]
+    knn = np.load(os.path.join(GOLD, "knn.npz"))
+    ps = core.PointSet.create(case["coords"], case["ids"])
+    tree = lt.build_local_tree(ps, lt.BuildConfig(**case["cfg"]))
+    k = case["ks"][0]
+    want = knn[f"u3_2000/k{k}/counters"]
+    for j in (0, 7, 19):
+        c = lq.count_visited(tree, case["queries"][j], k)
+        assert [c["nodes_visited"], c["buckets_scanned"], c["points_compared"]] == list(want[j])
+
+
+def _caterpillar(core, lt, n):
+    """A hand-made tree of depth n-1 (deeper than the fast kernels' fixed stack): node 2i splits
+    the sorted 2-D points at x_{i+1}, its left child is the one-point leaf {x_i}."""
+    xs = np.arange(n, dtype=np.float64) * 0.5 + np.linspace(0, 0.1, n)
+    coords = np.stack([xs, np.sin(np.arange(n))]).astype(np.float64)
+    ids = np.arange(100, 100 + n, dtype=np.uint64)
+    nn = 2 * n - 1
+    nd = np.full(nn, -1, np.int32); nv = np.zeros(nn); nl = np.zeros(nn, np.int32); nr = np.zeros(nn, np.int32)
+    nc = np.zeros(nn, np.int64)
+    for i in range(n - 1):
+        p = 2 * i
+        nd[p], nv[p], nl[p], nr[p], nc[p] = 0, xs[i + 1], p + 1, p + 2, n - i
+        nl[p + 1], nr[p + 1], nc[p + 1] = i, 1, 1  # leaf: (start, length)
+    nl[nn - 1], nr[nn - 1], nc[nn - 1] = n - 1, 1, 1
+    leaf = nd < 0
+    return lt.LocalTree(nd, nv, nl, nr, nc, core.PointSet(coords, ids), n - 1, nl[leaf].astype(np.int64),
+                        nr[leaf].astype(np.int64)), coords, ids
+
+
+def test_tree_deeper_than_the_fixed_stack(api, oracle):
+    """depth 59 > KNN_MAX_DEPTH: kd_knn falls back to the depth-sized walk (kd_walk.cu)."""
+    core, lt, lq = api
+    tree, coords, ids = _caterpillar(core, lt, 60)
+    q = np.random.default_rng(11).uniform([-1, -1], [31, 1], size=(500, 2))
+    for k, kw in ((1, {}), (5, {}), (40, {}), (5, dict(radii=4.0)), (3, dict(exclude_ids=np.full(500, 130, np.uint64)))):
+        d, i, c, _ = lq.find_knn_batch(tree, q, k, **kw)
+        sel = ids != 130 if "exclude_ids" in kw else np.ones(len(ids), bool)
+        bd, bi, bc = oracle.brute_knn(coords[:, sel], ids[sel], q, k, radii=kw.get("radii"))
+        assert np.array_equal(c, bc)
+        assert np.array_equal(masked(d, i, c)[0], masked(bd, bi, bc)[0])
+        assert np.array_equal(masked(d, i, c)[1], masked(bd, bi, bc)[1])
+
+
 def test_radius_queries(api, oracle):
     core, lt, lq = api
     for name in ("u3_2000", "f32_u3_20000"):

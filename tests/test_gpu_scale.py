@@ -111,7 +111,18 @@ def test_baseline_config_full_scale(torch_dev, oracle, cfgname):
     sel_t = torch.from_numpy(sel).to(dev)
     qs = queries[sel_t].cpu().numpy()
     kk = w.k + (1 if excl is not None else 0)
-    rd, ri, rc, _ = oracle.knn(ref, qs, kk)
+    rd, ri, rc, rctr = oracle.knn(ref, qs, kk)
+    # -- the device replay of the reference walk (KD_KNN_REFERENCE): rows AND counters equal the
+    #    reference traversal's, row for row (no tie-quirk allowance: it is the same walk)
+    from paper_1607_08220_b200 import _native as N
+    nw = nq if w.dims <= 3 else min(nq, 2000)  # 10-D walks compare ~1e5 points per query
+    wd, wi, wc, wctr = find_knn_device(tree, queries[sel_t[:nw]].contiguous(), kk, counters=True,
+                                       flags=N.KD_KNN_REFERENCE)
+    wd, wi, wc, wctr = wd.cpu().numpy(), wi.cpu().numpy().view(np.uint64), wc.cpu().numpy(), wctr.cpu().numpy()
+    assert np.array_equal(wc, rc[:nw]) and np.array_equal(wctr, rctr[:nw]), f"{cfgname}: reference-walk counters"
+    mw = np.arange(kk)[None, :] < wc[:, None]
+    assert np.array_equal(np.where(mw, wd, 0), np.where(mw, rd[:nw], 0)), f"{cfgname}: reference-walk distances"
+    assert np.array_equal(np.where(mw, wi, 0), np.where(mw, ri[:nw], 0)), f"{cfgname}: reference-walk ids"
     if excl is not None:
         ex = excl[sel_t].cpu().numpy().astype(np.uint64)
         rd, ri, rc = _drop_excluded(rd, ri, rc, ex, w.k)

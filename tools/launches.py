@@ -23,8 +23,8 @@ seq = list(launch.values())
 # the last step = the launches after the previous step's KNN kernel up to the last KNN kernel
 # (a query batch may launch several KNN kernels in a row: k_knn_home + k_knn_persist)
 kdbi = [i for i, e in enumerate(seq) if 'kdb::' in e['name']]
-knn = [i for n, i in enumerate(kdbi) if 'kdb::k_knn' in seq[i]['name']
-       and (n + 1 == len(kdbi) or 'kdb::k_knn' not in seq[kdbi[n + 1]]['name'])]
+isknn = lambda e: 'kdb::k_knn' in e['name'] and 'k_knn_walk' not in e['name']  # (the walk: counters, untimed)
+knn = [i for n, i in enumerate(kdbi) if isknn(seq[i]) and (n + 1 == len(kdbi) or not isknn(seq[kdbi[n + 1]]))]
 end = knn[-1]
 start = knn[-2] + 1 if len(knn) > 1 else 0
 seq = seq[:start] + [e for e in seq[start:end + 1] if 'kdb::' in e['name'] or 'CUB' in e['name']]
