@@ -71,7 +71,9 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampler running during the timed region (B200_PROFILING.md
+    clocks line).  NVML is polled from a thread every ~2 ms (a C1 timed region lasts a few ms,
+    shorter than nvidia-smi's start-up); nvidia-smi -lms 50 is the fallback."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -81,8 +83,47 @@ class Clocks:
         self.path = tempfile.mktemp(suffix=".csv")
         self.index = index
         self.proc = None
+        self.thread = None
+        self.rows = []
+        self.stop_flag = False
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        smax, pw, it = None, None, 0
+        while True:
+            try:
+                if it % 16 == 0:  # the slow queries only now and then: a C1 timed region lasts a few ms
+                    smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1e3
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.rows.append((float(sm), float(smax), pw, [k for k, b in bits.items() if rs & b]))
+            except Exception:
+                pass
+            it += 1
+            if self.stop_flag:
+                break
+            time.sleep(0.001)
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.stop_flag = False
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -91,6 +132,14 @@ class Clocks:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join(timeout=2)
+            sm = sorted(r[0] for r in self.rows)
+            reasons = sorted({x for r in self.rows for x in r[3]})
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.rows[-1][1] if self.rows else None,
+                    "samples": len(sm), "power_w_max": max((r[2] for r in self.rows), default=None),
+                    "reasons": reasons, "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -117,7 +166,7 @@ class Clocks:
         sm_load = sorted(sm)
         med = sm_load[len(sm_load) // 2] if sm_load else None
         return {"sm_mhz": med, "sm_max_mhz": smax, "samples": len(sm), "power_w_max": max(power) if power else None,
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "source": "nvidia-smi"}
 
 
 def build_bytes(n, dims, leaf):

@@ -1980,6 +1980,46 @@ static __global__ void k_top_pre(const LNode* lv, int K, TopStore ts, const int3
     ncount[p] = ts.npts[s];
 }
 
+// small trees: the whole stitch in one CTA (counts bottom-up, then preorder top-down, one
+// barrier per level) instead of two launches per level -- a 1M-point build spends 10 % of
+// its time in those launches
+constexpr int TOP_FUSED_LEVELS = 48;
+constexpr int TOP_FUSED_NODES = 16384;
+struct LevelList {
+    const LNode* lv[TOP_FUSED_LEVELS];
+    int k[TOP_FUSED_LEVELS];
+    int count;
+};
+static __global__ void __launch_bounds__(1024) k_top_count_all(LevelList L, TopStore ts, const int32_t* task_nodes) {
+    for (int l = L.count - 1; l >= 0; l--) {
+        for (int i = threadIdx.x; i < L.k[l]; i += blockDim.x) {
+            const int s = L.lv[l][i].slot;
+            if (ts.kind[s] != TS_INTERIOR) continue;
+            ts.nodes[s] = 1 + child_nodes(ts, task_nodes, ts.left[s]) + child_nodes(ts, task_nodes, ts.right[s]);
+        }
+        __syncthreads();
+    }
+}
+static __global__ void __launch_bounds__(1024) k_top_pre_all(LevelList L, TopStore ts, const int32_t* task_nodes,
+                                                             int32_t* task_base, KdNode* nodes, int32_t* ncount) {
+    for (int l = 0; l < L.count; l++) {
+        for (int i = threadIdx.x; i < L.k[l]; i += blockDim.x) {
+            const int s = L.lv[l][i].slot;
+            if (ts.kind[s] != TS_INTERIOR) continue;
+            const int p = ts.pre[s];
+            const int lc = ts.left[s], rc = ts.right[s];
+            const int pl = p + 1, pr = p + 1 + child_nodes(ts, task_nodes, lc);
+            ts.pre[lc] = pl;
+            ts.pre[rc] = pr;
+            if (ts.kind[lc] == TS_TASK) task_base[ts.task[lc]] = pl;
+            if (ts.kind[rc] == TS_TASK) task_base[ts.task[rc]] = pr;
+            nodes[p] = KdNode{ts.val[s], pr, ts.dim[s]};
+            ncount[p] = ts.npts[s];
+        }
+        __syncthreads();
+    }
+}
+
 static __global__ void k_relocate(const Task* tasks, const int32_t* task_nodes, const int32_t* task_base,
                            const KdNode* scratch, const int32_t* scnt, KdNode* nodes, int32_t* ncount) {
     const Task tk = tasks[blockIdx.x];
@@ -2395,8 +2435,19 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     KD_CUDA(cudaEventRecord(e_sub, st));
     tr.sync_mark(st, "k_subtree done", ntasks);
     // top counts bottom-up, preorder top-down
-    for (int L = (int)levels.size() - 1; L >= 0; L--)
-        k_top_count<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes);
+    size_t top_nodes = 0;
+    for (int kk : level_k) top_nodes += (size_t)kk;
+    const bool top_fused = levels.size() <= (size_t)TOP_FUSED_LEVELS && top_nodes <= (size_t)TOP_FUSED_NODES;
+    LevelList ll;
+    ll.count = 0;
+    if (top_fused) {
+        for (size_t L = 0; L < levels.size(); L++) { ll.lv[L] = levels[L]; ll.k[L] = level_k[L]; }
+        ll.count = (int)levels.size();
+        if (ll.count) k_top_count_all<<<1, 1024, 0, st>>>(ll, ts, task_nodes);
+    } else {
+        for (int L = (int)levels.size() - 1; L >= 0; L--)
+            k_top_count<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes);
+    }
     int32_t total_nodes = 0;
     {
         int32_t root_kind = 0;
@@ -2409,9 +2460,13 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     }
     KdNode* nodes = palloc<KdNode>(total_nodes, st);
     int32_t* ncount = palloc<int32_t>(total_nodes, st);
-    for (size_t L = 0; L < levels.size(); L++)
-        k_top_pre<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes, task_base, nodes,
-                                                            ncount);
+    if (top_fused) {
+        if (ll.count) k_top_pre_all<<<1, 1024, 0, st>>>(ll, ts, task_nodes, task_base, nodes, ncount);
+    } else {
+        for (size_t L = 0; L < levels.size(); L++)
+            k_top_pre<<<(level_k[L] + 255) / 256, 256, 0, st>>>(levels[L], level_k[L], ts, task_nodes, task_base, nodes,
+                                                                ncount);
+    }
     tr.sync_mark(st, "preorder done");
     k_relocate<<<ntasks, 256, 0, st>>>(tasks, task_nodes, task_base, scratch, scnt, nodes, ncount);
     tr.sync_mark(st, "relocate done");
