@@ -31,6 +31,16 @@ def test_library_exports_every_declared_symbol():
     assert N.lib.kd_version() >= 10000
 
 
+def test_flag_constants_match_header():
+    from paper_1607_08220_b200 import _native as N
+    src = open(os.path.join(ROOT, "include", "kdtree_b200.h")).read()
+    flags = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(KD_[A-Z_]+)\s+(\d+)u", src)}
+    assert flags == {"KD_DEVICE_PTRS": N.KD_DEVICE_PTRS, "KD_NO_SORT": N.KD_NO_SORT,
+                     "KD_THREAD_PER_QUERY": N.KD_THREAD_PER_QUERY, "KD_KNN_PACKET": N.KD_KNN_PACKET,
+                     "KD_KNN_REFERENCE": N.KD_KNN_REFERENCE}
+    assert len(set(flags.values())) == len(flags) and all(v & (v - 1) == 0 for v in flags.values())
+
+
 def test_library_is_sm100a():
     from paper_1607_08220_b200 import _native as N
     import subprocess
