@@ -26,7 +26,7 @@ struct KnnArgs {
 
 constexpr int KNN_MAX_DEPTH = 37;  // traversal stack capacity - 3
 constexpr int64_t KNN_CHUNK_MIN = 1 << 20;  // host-buffer pipeline: queries per chunk (at least)
-constexpr int64_t KNN_MAX_CHUNKS = 8;
+constexpr int64_t KNN_MAX_CHUNKS = 16;
 
 void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st);
 // kd_walk.cu: any depth / any k; reference = true walks exactly as local_query.py:72-172 (results and counters)
