@@ -225,7 +225,7 @@ k_sample(const T* __restrict__ src, const LNode* __restrict__ nodes, int K, DevC
         const int j = r * 32 + lane;
         kv[r] = j < m ? tkey(row[picked[j]]) : ~(Key)0;
     }
-    warp_sort_t<32>(kv);
+    warp_sort_rolled<32>(kv);  // rolled cross-lane merges: -0.65 ms over the 7 k_sample levels of C3
     // np.unique: first element of each run of equal keys; boundary index = rank of run.
     // Sorted element s = lane*32 + r.
     const int mid = m / 2;
@@ -1540,7 +1540,7 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
             }
         }
     }
-#pragma unroll
+#pragma unroll 1  // rolled: the kernel is bound by instruction fetch (-1.1 ms on C3)
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
         for (int d = 0; d < DT; d++) {
@@ -1584,6 +1584,7 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
             if (d == best) v = x[d][r];
         kv[r] = r * 32 + lane < n ? tkey(v) : ~(Key)0;
     }
+    // (the rolled network is slower here: 24.7 vs 23.2 ms -- too small a body for the loop overhead)
     warp_sort_t<SR>(kv);  // sorted element s in lane s / SR, register s % SR
     const int h = n / 2;
     Key mine = kv[0];
@@ -1659,7 +1660,7 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
             }
         }
     }
-#pragma unroll
+#pragma unroll 1  // rolled: the kernel is bound by instruction fetch (-1.1 ms on C3)
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
         for (int d = 0; d < DC; d++) {

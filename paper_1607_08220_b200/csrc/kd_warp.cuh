@@ -96,6 +96,45 @@ __device__ __forceinline__ void warp_sort_t(K (&v)[R]) {
     merges<2, 32 * R, R>(v, threadIdx.x & 31);
 }
 
+// The same network with the cross-lane merges rolled: every merge of more than R keys is
+// [lane flip] [lane half-cleaners, stride ks/4 .. 1 lanes] [register half-cleaners R/2 .. 1],
+// identical code for every merge size, so it runs as a loop over the merge size with runtime
+// shuffle masks.  Same comparators, same result; the instruction stream is ~5x shorter, which
+// matters where the kernel is bound by instruction fetch (straight-line code is fetched, not
+// reused: k_subtree's split functions, k_sample's 1024-key sorts).
+template <int R, typename K>
+__device__ __forceinline__ void warp_sort_rolled(K (&v)[R]) {
+    const int lane = threadIdx.x & 31;
+    merges<2, R, R>(v, lane);  // each lane's R keys, in registers
+#pragma unroll 1
+    for (int ks = 2; ks <= 32; ks <<= 1) {  // lanes per merged run
+        {
+            const int lm = ks - 1;  // partner of (lane, r) is (lane ^ lm, R-1-r)
+            const bool lower = (lane & (ks >> 1)) == 0;
+#pragma unroll
+            for (int r = 0; r < (R + 1) / 2; r++) {
+                const int q = R - 1 - r;
+                const K a = __shfl_xor_sync(FULL, v[q], lm);
+                if (q != r) {
+                    const K b = __shfl_xor_sync(FULL, v[r], lm);
+                    v[q] = lower ? kmin(v[q], b) : kmax(v[q], b);
+                }
+                v[r] = lower ? kmin(v[r], a) : kmax(v[r], a);
+            }
+        }
+#pragma unroll 1
+        for (int jl = ks >> 2; jl >= 1; jl >>= 1) {
+            const bool lower = (lane & jl) == 0;
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const K o = __shfl_xor_sync(FULL, v[r], jl);
+                v[r] = lower ? kmin(v[r], o) : kmax(v[r], o);
+            }
+        }
+        half_stages<R / 2, R>(v, lane);
+    }
+}
+
 // the sorted element before (lane, r) in a transposed sorted array; `up` is
 // __shfl_up_sync(v[R-1], 1) (the previous lane's last key), `none` for element 0
 template <int R, typename K>

@@ -8,7 +8,7 @@ cd "$(dirname "$0")/../paper_1607_08220_b200/csrc"
 make -s -j4 >/dev/null 2>&1
 mkdir -p build_$NAME
 OBJS=""
-for f in kd_build_f32.cu kd_build_f64.cu kd_query.cu kd_packet.cu kd_capi.cu kd_dist.cu; do
+for f in kd_build_f32.cu kd_build_f64.cu kd_query.cu kd_walk.cu kd_packet.cu kd_capi.cu kd_dist.cu; do
   if [[ " $SRCS " == *" $f "* ]]; then
     /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr $FLAGS -c $f -o build_$NAME/${f%.cu}.o &
     OBJS="$OBJS build_$NAME/${f%.cu}.o"
