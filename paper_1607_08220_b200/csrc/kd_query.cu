@@ -39,6 +39,7 @@ namespace kdb {
 // therefore always true (they stay: without them nvcc schedules the persistent
 // kernel's push ~5 % slower on C2/C3, measured)
 constexpr int QCAP = 40;
+constexpr int KNN_MORTON_BITS = 32;  // Morton key bits of the 3-D query order
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
 // (measured 34 vs 44 ms on C2); in higher dimensions the binary64 leaf scan dominates and it pays off
 template <int DT>
@@ -1126,7 +1127,7 @@ __device__ __forceinline__ uint32_t spread11(uint32_t x) {  // 11 bits -> every 
 }
 
 static __global__ void k_morton(const double* __restrict__ q, int64_t nq, const unsigned long long* __restrict__ box,
-                                uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+                                uint32_t* __restrict__ key, int32_t* __restrict__ val, int drop) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= nq) return;
     uint32_t c[3];
@@ -1139,7 +1140,7 @@ static __global__ void k_morton(const double* __restrict__ q, int64_t nq, const 
     }
     // 32-bit key: x and y with 11 bits, z with 10 (its lowest bit dropped)
     const uint64_t k = ((uint64_t)spread11(c[0]) << 2) | ((uint64_t)spread11(c[1]) << 1) | (uint64_t)spread11(c[2]);
-    key[i] = (uint32_t)(k >> 1);
+    key[i] = (uint32_t)(k >> drop);  // the top 33 - drop bits of the interleaved key
     val[i] = (int32_t)i;
 }
 
@@ -1172,9 +1173,13 @@ void knn(const KdTreeDev& t, const KnnArgs& a, cudaStream_t st) {
             const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
             KD_CUDA(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, st));
             k_qbox<<<592, 256, 0, st>>>(a.queries, a.nq, box);
-            k_morton<<<(unsigned)((a.nq + 255) / 256), 256, 0, st>>>(a.queries, a.nq, box, k0, v0);
+            static const int mbits = [] {  // key bits = radix-sort passes * 8 (KDB_MORTON_BITS: A/B)
+                const char* e = getenv("KDB_MORTON_BITS");
+                return e ? std::min(32, std::max(8, atoi(e))) : KNN_MORTON_BITS;
+            }();
+            k_morton<<<(unsigned)((a.nq + 255) / 256), 256, 0, st>>>(a.queries, a.nq, box, k0, v0, 33 - mbits);
             scratch_free(box, st);
-            bits = 32;
+            bits = mbits;
         } else {
             const unsigned blocks = (unsigned)((a.nq + 1023) / 1024);  // 4 queries per thread
             if (t.dims == 3) k_leaf_of<3><<<blocks, 256, 0, st>>>(t.nodes, t.n_nodes, a.queries, t.dims, a.nq, k0, v0);
