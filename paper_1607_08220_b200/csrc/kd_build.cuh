@@ -2211,6 +2211,14 @@ void build_tree(const T* d_in, const uint64_t* d_ids, int64_t n, int dims, const
     T* buf[2] = {palloc<T>((size_t)dims * n, st), dalloc<T>((size_t)dims * n, st)};
     int32_t* idx[2] = {palloc<int32_t>(n, st), dalloc<int32_t>(n, st)};
 
+    // the bulk-copy (TMA) tile loads start at the 16-byte boundary below a tile: a caller's buffer
+    // that is not 16-byte aligned (a view into a larger tensor) is first copied into build scratch
+    if (reinterpret_cast<uintptr_t>(d_in) & 15) {
+        T* aligned = dalloc<T>((size_t)dims * n, st);
+        KD_CUDA(cudaMemcpyAsync(aligned, d_in, sizeof(T) * (size_t)dims * n, cudaMemcpyDeviceToDevice, st));
+        d_in = aligned;
+    }
+
     // top store (grown per level)
     size_t ts_cap = 1024;
     TopStore ts{};

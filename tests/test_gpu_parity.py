@@ -180,6 +180,24 @@ def test_tree_deeper_than_the_fixed_stack(api, oracle):
         assert np.array_equal(masked(d, i, c)[1], masked(bd, bi, bc)[1])
 
 
+def test_misaligned_device_input(oracle):
+    """A device buffer that is only 4-byte aligned (a view one element into a tensor): the TMA tile
+    loads need 16-byte-aligned sources, so the build copies such an input first."""
+    import torch
+    from paper_1607_08220_b200.local_tree import BuildConfig, build_local_tree_device
+    n = 70001
+    rows = make_rows(n, 3, 9, "f32")
+    flat = torch.empty(3 * n + 1, dtype=torch.float32, device="cuda")
+    view = flat[1:].view(3, n)
+    view.copy_(torch.from_numpy(np.ascontiguousarray(rows.T.astype(np.float32))))
+    assert view.data_ptr() % 16 == 4 and view.is_contiguous()
+    tree = build_local_tree_device(view, None, BuildConfig(bucket_size=32, seed=3))
+    ref = oracle.build_tree(np.ascontiguousarray(rows.T), bucket_size=32, seed=3)
+    for f in ("node_dim", "node_value", "node_left", "node_right", "node_count"):
+        assert np.array_equal(getattr(tree, f), getattr(ref, f)), f
+    assert np.array_equal(tree.points.ids, ref.ids)
+
+
 def test_radius_queries(api, oracle):
     core, lt, lq = api
     for name in ("u3_2000", "f32_u3_20000"):
