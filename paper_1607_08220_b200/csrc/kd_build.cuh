@@ -1517,8 +1517,11 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
 #pragma unroll
         for (int d = 0; d < DT; d++) x[d][r] = cs[d * ts + q];
     }
-    // per dimension: min/max key (constant?), shifted binary64 sums; the four
-    // reductions of every dimension run interleaved (one butterfly)
+    // per dimension: constant?, shifted binary64 sums (y = x - x0); the reductions of every
+    // dimension run interleaved (one butterfly).  A float dimension is constant exactly when
+    // sum y^2 == 0 (y == 0 iff x == x0, and a float difference squared cannot underflow in
+    // binary64), so only double coordinates need the min / max keys.
+    constexpr bool KEYS = sizeof(T) != 4;
     Key kmn[DT], kmx[DT];
     double s1[DT], sq[DT];
 #pragma unroll
@@ -1531,9 +1534,11 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
 #pragma unroll
         for (int r = 0; r < SR; r++) {
             if (r * 32 + lane < n) {
-                const Key k = tkey(x[d][r]);
-                kmn[d] = k < kmn[d] ? k : kmn[d];
-                kmx[d] = k > kmx[d] ? k : kmx[d];
+                if constexpr (KEYS) {
+                    const Key k = tkey(x[d][r]);
+                    kmn[d] = k < kmn[d] ? k : kmn[d];
+                    kmx[d] = k > kmx[d] ? k : kmx[d];
+                }
                 const double y = __dsub_rn((double)x[d][r], x0);
                 s1[d] = __dadd_rn(s1[d], y);
                 sq[d] = __dadd_rn(sq[d], __dmul_rn(y, y));
@@ -1544,9 +1549,11 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
         for (int d = 0; d < DT; d++) {
-            const Key a = __shfl_xor_sync(FULL, kmn[d], o), b = __shfl_xor_sync(FULL, kmx[d], o);
-            kmn[d] = a < kmn[d] ? a : kmn[d];
-            kmx[d] = b > kmx[d] ? b : kmx[d];
+            if constexpr (KEYS) {
+                const Key a = __shfl_xor_sync(FULL, kmn[d], o), b = __shfl_xor_sync(FULL, kmx[d], o);
+                kmn[d] = a < kmn[d] ? a : kmn[d];
+                kmx[d] = b > kmx[d] ? b : kmx[d];
+            }
             s1[d] = __dadd_rn(s1[d], __shfl_xor_sync(FULL, s1[d], o));
             sq[d] = __dadd_rn(sq[d], __shfl_xor_sync(FULL, sq[d], o));
         }
@@ -1560,7 +1567,7 @@ __device__ __noinline__ void sub_split_small(const T* cs, const uint16_t* pm, in
     for (int d = 0; d < DT; d++) {
         s2v[d] = 0.0;
         eb[d] = 0.0;
-        if (kmn[d] == kmx[d]) continue;
+        if (KEYS ? kmn[d] == kmx[d] : sq[d] == 0.0) continue;
         ncmask |= 1u << d;
         const double bb = __dmul_rn(__dmul_rn(s1[d], s1[d]), rn);
         s2v[d] = sq[d] - bb;
