@@ -1638,15 +1638,24 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
     // pass over the node reads each point's index once for every dimension
     // (shifted sums y = x - x0, x0 = the node's first point; S2 = sum y^2 - (sum y)^2 / n),
     // then the reductions of all dimensions run interleaved.
-    Key kmins[DC], kmaxs[DC];
+    // (float coordinates: the min / max run on the values themselves -- one FMNMX each instead of
+    //  a key conversion per element -- and become keys after the reduction)
+    constexpr bool FVAL = sizeof(T) == 4;
+    typedef typename std::conditional<FVAL, float, Key>::type MM;
+    MM kmins[DC], kmaxs[DC];
     double s1[DC], sq[DC], x0[DC];
     {
         const int q0 = pm[0];
 #pragma unroll
         for (int d = 0; d < DC; d++) {
             x0[d] = d < D ? (double)cs[d * ts + q0] : 0.0;
-            kmins[d] = ~(Key)0;
-            kmaxs[d] = 0;
+            if constexpr (FVAL) {
+                kmins[d] = INFINITY;
+                kmaxs[d] = -INFINITY;
+            } else {
+                kmins[d] = ~(Key)0;
+                kmaxs[d] = 0;
+            }
             s1[d] = 0.0;
             sq[d] = 0.0;
         }
@@ -1658,9 +1667,14 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
         for (int d = 0; d < DC; d++) {
             if (d < D) {
                 const T v = cs[d * ts + qv];
-                const Key k = tkey(v);
-                kmins[d] = k < kmins[d] ? k : kmins[d];
-                kmaxs[d] = k > kmaxs[d] ? k : kmaxs[d];
+                if constexpr (FVAL) {
+                    kmins[d] = fminf(kmins[d], (float)v);
+                    kmaxs[d] = fmaxf(kmaxs[d], (float)v);
+                } else {
+                    const Key k = tkey(v);
+                    kmins[d] = k < kmins[d] ? k : kmins[d];
+                    kmaxs[d] = k > kmaxs[d] ? k : kmaxs[d];
+                }
                 const double y = __dsub_rn((double)v, x0[d]);
                 s1[d] = __dadd_rn(s1[d], y);
                 sq[d] = __dadd_rn(sq[d], __dmul_rn(y, y));
@@ -1672,9 +1686,14 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
 #pragma unroll
         for (int d = 0; d < DC; d++) {
             if (d < D) {
-                const Key a = __shfl_xor_sync(FULL, kmins[d], o), b = __shfl_xor_sync(FULL, kmaxs[d], o);
-                kmins[d] = a < kmins[d] ? a : kmins[d];
-                kmaxs[d] = b > kmaxs[d] ? b : kmaxs[d];
+                const MM a = __shfl_xor_sync(FULL, kmins[d], o), b = __shfl_xor_sync(FULL, kmaxs[d], o);
+                if constexpr (FVAL) {
+                    kmins[d] = fminf(kmins[d], a);
+                    kmaxs[d] = fmaxf(kmaxs[d], b);
+                } else {
+                    kmins[d] = a < kmins[d] ? a : kmins[d];
+                    kmaxs[d] = b > kmaxs[d] ? b : kmaxs[d];
+                }
                 s1[d] = __dadd_rn(s1[d], __shfl_xor_sync(FULL, s1[d], o));
                 sq[d] = __dadd_rn(sq[d], __shfl_xor_sync(FULL, sq[d], o));
             }
@@ -1708,10 +1727,18 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
     if (!certified) best = sub_exact_dim<T>(cs, pm, n, ts, D, ncmask, path, c, fyslots, fylocks);
     Key ks, nxt;
     int lt, eq;
-    Key bmin = kmins[0], bmax = kmaxs[0];
+    MM mmin = kmins[0], mmax = kmaxs[0];
 #pragma unroll
     for (int d = 1; d < DC; d++)
-        if (d == best) { bmin = kmins[d]; bmax = kmaxs[d]; }
+        if (d == best) { mmin = kmins[d]; mmax = kmaxs[d]; }
+    Key bmin, bmax;
+    if constexpr (FVAL) {
+        bmin = tkey((T)mmin);
+        bmax = tkey((T)mmax);
+    } else {
+        bmin = mmin;
+        bmax = mmax;
+    }
     warp_select<T>(cs + best * ts, pm, n, n / 2, hist, bmin, bmax, ks, lt, eq, nxt);
     const int cumA = lt, cumB = lt + eq;
     bool pickB;
