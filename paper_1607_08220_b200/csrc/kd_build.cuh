@@ -1358,15 +1358,15 @@ __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
     return b;
 }
 
-// k-th smallest key (0-based) of the node's values + below/equal counts and the
-// next larger key.  Keys are read from shared memory through the node's
-// permutation (runtime loops: small code, few registers); 8-bit digit radix
-// select with a per-warp shared-memory histogram.
+// k-th smallest key (0-based) of the node's values + below/equal counts.  Keys are read from
+// shared memory through the node's permutation (runtime loops: small code, few registers);
+// 8-bit digit radix select with a per-warp shared-memory histogram.  The counts fall out of
+// the passes: the rank left inside the last digit's bin is the key's rank among its equals,
+// so lt = kth - rem and eq = that bin's count (no counting pass over the node).
 template <typename T>
 __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, int n, int kth, uint32_t* hist,
                                             typename KeyOf<T>::type kmin_, typename KeyOf<T>::type kmax_,
-                                            typename KeyOf<T>::type& ks, int& lt, int& eq,
-                                            typename KeyOf<T>::type& nxt) {
+                                            typename KeyOf<T>::type& ks, int& lt, int& eq) {
     typedef typename KeyOf<T>::type Key;
     row = as_dyn_shared(row);
     pm = as_dyn_shared(pm);
@@ -1380,6 +1380,7 @@ __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, in
     const int start = (top / 8) * 8;
     Key prefix = start + 8 >= KB ? (Key)0 : (kmin_ & ((~(Key)0) << (start + 8)));
     int rem = kth;
+    int bin = n;  // keys in the selected bin of the last pass
 #pragma unroll 1
     for (int shift = start; shift >= 0; shift -= 8) {
         for (int i = lane; i < 256; i += 32) hist[i] = 0;
@@ -1403,39 +1404,51 @@ __device__ __forceinline__ void warp_select(const T* row, const uint16_t* pm, in
         }
         const uint32_t excl = incl - s;
         const bool mine = (uint32_t)rem >= excl && (uint32_t)rem < incl;
-        int digit = 0, newrem = 0;
+        int digit = 0, newrem = 0, cnt = 0;
         if (mine) {
             uint32_t acc = excl;
 #pragma unroll
             for (int j = 0; j < 8; j++) {
-                if ((uint32_t)rem >= acc && (uint32_t)rem < acc + h[j]) { digit = lane * 8 + j; newrem = rem - (int)acc; }
+                if ((uint32_t)rem >= acc && (uint32_t)rem < acc + h[j]) {
+                    digit = lane * 8 + j;
+                    newrem = rem - (int)acc;
+                    cnt = (int)h[j];
+                }
                 acc += h[j];
             }
         }
         const int src = __ffs(__ballot_sync(FULL, mine)) - 1;
         digit = __shfl_sync(FULL, digit, src);
         rem = __shfl_sync(FULL, newrem, src);
+        bin = __shfl_sync(FULL, cnt, src);
         prefix |= ((Key)digit) << shift;
         __syncwarp();
     }
     ks = prefix;
-    int l = 0, e = 0;
+    lt = kth - rem;
+    eq = bin;
+}
+
+// smallest key above ks (only needed when the split takes the next boundary)
+template <typename T>
+__device__ __forceinline__ typename KeyOf<T>::type warp_next_key(const T* row, const uint16_t* pm, int n,
+                                                                 typename KeyOf<T>::type ks) {
+    typedef typename KeyOf<T>::type Key;
+    row = as_dyn_shared(row);
+    pm = as_dyn_shared(pm);
+    const int lane = threadIdx.x & 31;
     Key nx = ~(Key)0;
 #pragma unroll 4
     for (int i = lane; i < n; i += 32) {
         const Key kk = tkey(row[pm[i]]);
-        l += kk < ks;
-        e += kk == ks;
         if (kk > ks && kk < nx) nx = kk;
     }
-    lt = warp_isum(l);
-    eq = warp_isum(e);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const Key on = __shfl_xor_sync(FULL, nx, o);
         nx = on < nx ? on : nx;
     }
-    nxt = nx;
+    return nx;
 }
 
 static __device__ __noinline__ void fy_resolve_n(uint32_t n, uint64_t seed, uint32_t* fk, uint32_t* fp) {
@@ -1725,7 +1738,7 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
     for (int d = 0; d < DC; d++)
         if (d != best && ((ncmask >> d) & 1u) && !(bs - s2v[d] > be + eb[d])) certified = false;
     if (!certified) best = sub_exact_dim<T>(cs, pm, n, ts, D, ncmask, path, c, fyslots, fylocks);
-    Key ks, nxt;
+    Key ks;
     int lt, eq;
     MM mmin = kmins[0], mmax = kmaxs[0];
 #pragma unroll
@@ -1739,14 +1752,15 @@ __device__ __noinline__ void sub_split(const T* cs, const uint16_t* pm, int n, i
         bmin = mmin;
         bmax = mmax;
     }
-    warp_select<T>(cs + best * ts, pm, n, n / 2, hist, bmin, bmax, ks, lt, eq, nxt);
+    warp_select<T>(cs + best * ts, pm, n, n / 2, hist, bmin, bmax, ks, lt, eq);
     const int cumA = lt, cumB = lt + eq;
     bool pickB;
     if (cumA == 0) pickB = true;          // A is the first boundary (diff 0.5)
     else if (cumB >= n) pickB = false;    // no boundary after A
     else pickB = closer_to_half(cumB, cumA, n);
     out_dim = best;
-    out_val = pickB ? (double)key_inv(nxt, (T*)nullptr) : (double)key_inv(ks, (T*)nullptr);
+    out_val = pickB ? (double)key_inv(warp_next_key<T>(cs + best * ts, pm, n, ks), (T*)nullptr)
+                    : (double)key_inv(ks, (T*)nullptr);
     out_nl = pickB ? cumB : cumA;
 }
 
