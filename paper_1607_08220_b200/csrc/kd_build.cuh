@@ -1038,7 +1038,10 @@ k_scatter(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __rest
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent: a grid of resident CTAs strides over the half-tiles (empty second
     // halves of small nodes cost a loop iteration, not a CTA launch)
-    for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x) {
+    // a contiguous run per CTA: the empty second halves of small nodes sit at every other index
+    const uint32_t h0 = (uint32_t)((uint64_t)nhalf * blockIdx.x / gridDim.x);
+    const uint32_t h1 = (uint32_t)((uint64_t)nhalf * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t hb = h0; hb < h1; hb++) {
     const HalfMeta hm = meta[hb];
     if (hm.e1 <= hm.e0) continue;  // not split, or the empty second half of a small node
     const int64_t e0 = hm.e0, e1 = hm.e1;
@@ -1187,14 +1190,30 @@ k_scatter_tma(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __
                          : "memory");
         }
     };
-    if (threadIdx.x == 0 && blockIdx.x < nhalf) issue(blockIdx.x, 0);
+    // each CTA takes a contiguous run of half-tiles (the empty second halves of nodes of <= 2048
+    // points sit at every other index: a strided walk would hand them all to every other CTA)
+    // and skips the empty ones; stages / parities advance with the non-empty ones only
+    const uint32_t h0 = (uint32_t)((uint64_t)nhalf * blockIdx.x / gridDim.x);
+    const uint32_t h1 = (uint32_t)((uint64_t)nhalf * (blockIdx.x + 1) / gridDim.x);
+    auto next_work = [&](uint32_t from) {  // first non-empty half-tile in [from, h1), or h1
+        while (from < h1 && meta[from].e1 <= meta[from].e0) from++;
+        return from;
+    };
+    if (threadIdx.x == 0) {
+        const uint32_t f = next_work(h0);
+        if (f < h1) issue(f, 0);
+    }
     uint32_t it = 0;
-    for (uint32_t hb = blockIdx.x; hb < nhalf; hb += gridDim.x, it++) {
-        const int slot = it & 1;
-        if (threadIdx.x == 0 && hb + gridDim.x < nhalf) issue(hb + gridDim.x, slot ^ 1);
+    for (uint32_t hb = h0; hb < h1; hb++) {
         const HalfMeta hm = meta[hb];
-        mbar_wait(&mbar[slot], (it >> 1) & 1);  // this half-tile's bytes have landed (0 bytes: at once)
-        if (hm.e1 > hm.e0) {
+        if (hm.e1 <= hm.e0) continue;  // not split, or the empty second half of a small node
+        const int slot = it & 1;
+        if (threadIdx.x == 0) {
+            const uint32_t f = next_work(hb + 1);
+            if (f < h1) issue(f, slot ^ 1);
+        }
+        mbar_wait(&mbar[slot], (it >> 1) & 1);  // this half-tile's bytes have landed
+        {
             const int cnt = hm.e1 - hm.e0;
             const int64_t gbase = hm.gbase;
             const uint32_t lbefore = tile_loff[hb] - tile_loff[hm.first_hb];  // lefts earlier in this node
@@ -1256,6 +1275,7 @@ k_scatter_tma(const T* __restrict__ src, const int32_t* __restrict__ isrc, T* __
             }
         }
         __syncthreads();  // the stage is free for the copy issued two iterations on; wl / wpre reusable
+        it++;
     }
 }
 
