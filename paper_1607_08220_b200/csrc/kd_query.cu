@@ -38,6 +38,9 @@ namespace kdb {
 // push can never overflow; the `sp < QCAP` terms in the push conditions are
 // therefore always true (they stay: without them nvcc schedules the persistent
 // kernel's push ~5 % slower on C2/C3, measured)
+#ifndef KD_KNN_CTAS
+#define KD_KNN_CTAS 7
+#endif
 constexpr int QCAP = 40;
 constexpr int KNN_MORTON_BITS = 32;  // Morton key bits of the 3-D query order
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
@@ -371,7 +374,7 @@ k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restric
 //       2 = two-pass: the k-th distance bound comes from k_knn_home (bound0, by sorted position),
 //           and buckets are scanned in chunks whose hits are inserted afterwards (see below)
 template <typename T, int DT, int KM, int SCAN = 0>
-__global__ void __launch_bounds__(128, (DT > 0 && DT <= 3 && KM <= 8) ? 7 : 1)
+__global__ void __launch_bounds__(128, (DT > 0 && DT <= 3 && KM <= 8) ? KD_KNN_CTAS : 1)
 k_knn_persist(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restrict__ coords,
               const uint64_t* __restrict__ ids, int64_t n, int dims_rt, const double* __restrict__ queries,
               const int32_t* __restrict__ order, int64_t nq, int k, const double* __restrict__ radii,
