@@ -12,17 +12,18 @@
 // GPU structure:
 //   breadth-first levels for nodes larger than the sample size (global memory,
 //   SoA coordinates ping-ponged between two buffers):
-//     k_sample   warp/node  exact Fisher-Yates draws, certified variance order,
-//                           sorted unique median sample, 256-boundary window
+//     k_sample   warp/node  exact Fisher-Yates draws (direct / hash table), certified
+//                           variance order, sorted unique median sample, 128-boundary window
 //     k_hist     tile/CTA   windowed full-data histogram of the split dim
 //     k_select   warp/node  exact binary64 median selection from the window
 //     k_slow     CTA/node   exact slow path (full histogram, exact fallback,
 //                           next dimensions) -- only for flagged nodes
-//     k_tile_left/scan/k_scatter  stable segmented partition of coords + row ids
-//                           (per-half-tile left counts from k_hist's window rows)
+//     k_tile_left/scan/k_scatter_tma (k_scatter for D > 3)  stable segmented partition of
+//                           coords + row ids, TMA-fed (per-half-tile left counts from
+//                           k_hist's window rows)
 //     k_children thread/node child records, next level, subtree tasks
-//   then one CTA per subtree of <= min(1024, samples) points, built entirely in
-//   shared memory (k_subtree), and a preorder stitch (k_top_* / k_relocate).
+//   then one CTA (two warps) per subtree of <= min(1024, samples) points, built entirely
+//   in shared memory (k_subtree), and a preorder stitch (k_top_* / k_relocate).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1366,8 +1367,8 @@ struct SubStack {
     uint32_t packed;     // start (10 bits) | n (11 bits) << 10 | rel depth (11 bits) << 21
 };
 
-constexpr int FY_SLOTS = 8192;
-constexpr int SUB_WARPS_HOST = 2;  // == SUB_WARPS (k_subtree)  // global scratch slots for the rare exact-variance path
+constexpr int FY_SLOTS = 8192;  // global scratch slots for the rare exact-variance path
+constexpr int SUB_WARPS_HOST = 2;  // == SUB_WARPS (k_subtree)
 
 __host__ __device__ inline size_t sub_smem_bytes(int ts, int dims, int tsize) {
     size_t b = (size_t)dims * ts * tsize;
@@ -1896,16 +1897,9 @@ k_subtree(const Task* __restrict__ tasks, T* buf0, const T* buf1, const T* in0, 
         if (nn > c.bucket) {
             const uint16_t* pmn = ((rd & 1) ? perm[1] : perm[0]) + st;
             if constexpr (DT > 0) {
-#if defined(KD_SUB_NO_SMALL)
-                sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
-#elif defined(KD_SUB_NO_SMALL4)
-                if (nn <= 64) sub_split_small<T, DT, 2>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
-                else sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
-#else
                 if (nn <= 64) sub_split_small<T, DT, 2>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
                 else if (nn <= 128) sub_split_small<T, DT, 4>(cs, pmn, nn, ts, path, c, fyslots, fylocks, dim, val, nl);
                 else sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
-#endif
             } else {
                 sub_split<T, DT>(cs, pmn, nn, ts, D, path, c, hist, fyslots, fylocks, dim, val, nl);
             }
