@@ -494,8 +494,16 @@ def rank_build_global(comm, pts: DevicePoints, cfg: ClusterConfig, backend=_CUDA
         reg = gt.region_of(me)
         lo = torch.as_tensor(reg.lower, device=pts.coords.device)[:, None]
         hi = torch.as_tensor(reg.upper, device=pts.coords.device)[:, None]
-        c = pts.coords.double()
-        if not bool(((c >= lo) & (c <= hi)).all()):
+        c = pts.coords
+        if c.dtype != torch.float64:
+            # region bounds are split values, i.e. coordinates: when they are exact in the storage type
+            # the check runs on the stored values (no binary64 copy of the rank's points per build)
+            lo_c, hi_c = lo.to(c.dtype), hi.to(c.dtype)
+            if bool((lo_c.double() == lo).all()) and bool((hi_c.double() == hi).all()):
+                lo, hi = lo_c, hi_c
+            else:
+                c = c.double()
+        if bool(((c < lo) | (c > hi)).any()):
             raise AssertionError(f"rank {me}: point outside its region after redistribution")
     return gt, pts, stats
 
