@@ -340,6 +340,25 @@ def test_big_root_node_tree_parity(api, oracle):
     assert np.array_equal(tree.points.ids, ref.ids) and tree.depth == ref.depth
 
 
+@pytest.mark.parametrize("dims,kind,n,seed", [(3, "uniform", 6_000_000, 31), (2, "f32", 6_000_000, 32)])
+def test_large_trees_binary64_and_2d(api, oracle, dims, kind, n, seed):
+    """6M points that are NOT binary32-exact (binary64 storage: k_sample / fy_hash / k_scatter_tma
+    instantiated for double) and 6M 2-D float points (the 2-D TMA partition): breadth-first levels
+    with more than 1024 nodes of more than 4096 points, whole tree byte-equal to the oracle."""
+    core, lt, lq = api
+    rows = make_rows(n, dims, seed, kind)
+    ps = core.PointSet.from_rows(rows)
+    tree = lt.build_local_tree(ps, lt.BuildConfig(seed=seed))
+    ref = oracle.build_tree(ps.coords, ps.ids, seed=seed)
+    for key in ("node_dim", "node_value", "node_left", "node_right", "node_count"):
+        assert np.array_equal(getattr(tree, key), getattr(ref, key)), key
+    assert np.array_equal(tree.points.ids, ref.ids) and tree.depth == ref.depth
+    q = make_rows(2000, dims, seed + 1, kind)
+    d, i, c, _ = lq.find_knn_batch(tree, q, 5)
+    bd, bi, bc = oracle.brute_knn(ps.coords, ps.ids, q, 5)
+    assert np.array_equal(c, bc) and np.array_equal(d, bd) and np.array_equal(i, bi)
+
+
 def test_large_duplicate_heavy_tree_parity(api, oracle):
     """1.5M points, 40 % of them stacked on 50 sites: degenerate breadth-first nodes,
     constant dimensions, exact-fallback splits -- tree byte-equal, KNN equal to brute force."""
