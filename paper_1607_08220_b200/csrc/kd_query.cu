@@ -41,6 +41,9 @@ namespace kdb {
 #ifndef KD_KNN_CTAS
 #define KD_KNN_CTAS 7
 #endif
+#ifndef KD_HOME_F32
+#define KD_HOME_F32 1
+#endif
 constexpr int QCAP = 40;
 constexpr int KNN_MORTON_BITS = 32;  // Morton key bits of the 3-D query order
 // the fp32 pre-filter costs the persistent kernel more in registers/occupancy than it saves in 2-3 D
@@ -302,10 +305,58 @@ k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restric
         rec = nodes[node];
     }
     const int start = rec.a, end = rec.a + (-1 - rec.db);
+    constexpr int UN = 4;
+    double b;
+    if constexpr (sizeof(T) == 4 && KD_HOME_F32) {
+        // float coordinates: the bound only has to be an UPPER bound on the kk-th distance, so it is
+        // computed in fp32 with upward rounding -- |c - q| <= max(c - q_lo, q_hi - c) with q_lo <= q
+        // <= q_hi the float neighbours of q, squares accumulated by round-up FMAs -- one FMNMX per
+        // step of the selection chain instead of compare + selects on doubles.  Points enter when the
+        // upper bound is below the radius rounded down, so the bound stays below the radius.
+        float qlo[DT], qhi[DT];
+#pragma unroll
+        for (int d = 0; d < DT; d++) {
+            qlo[d] = __double2float_rd(q[d]);
+            qhi[d] = __double2float_ru(q[d]);
+        }
+        const float radf = __double2float_rd(radius);
+        float fd[KM];
+#pragma unroll
+        for (int j = 0; j < KM; j++) fd[j] = INFINITY;
+        for (int base = start; base < end; base += UN) {
+            float cv[UN][DT];
+#pragma unroll
+            for (int u = 0; u < UN; u++) {
+                const int i = min(base + u, end - 1);
+#pragma unroll
+                for (int d = 0; d < DT; d++) cv[u][d] = (float)coords[(int64_t)d * n + i];
+            }
+#pragma unroll
+            for (int u = 0; u < UN; u++) {
+                float ub = 0.0f;
+#pragma unroll
+                for (int d = 0; d < DT; d++) {
+                    const float m = fmaxf(__fsub_ru(cv[u][d], qlo[d]), __fsub_ru(qhi[d], cv[u][d]));
+                    ub = __fmaf_ru(m, m, ub);
+                }
+                float x = (base + u < end && ub < radf) ? ub : INFINITY;
+#pragma unroll
+                for (int j = 0; j < KM; j++) {
+                    const float lo = fminf(x, fd[j]);
+                    x = fmaxf(x, fd[j]);
+                    fd[j] = lo;
+                }
+            }
+        }
+        float bf = fd[KM - 1];
+#pragma unroll
+        for (int j = 0; j < KM - 1; j++)
+            if (j == kk - 1) bf = fd[j];
+        b = (double)bf;
+    } else {
     double bd[KM];
 #pragma unroll
     for (int j = 0; j < KM; j++) bd[j] = INFINITY;
-    constexpr int UN = 4;
     for (int base = start; base < end; base += UN) {
         T cv[UN][DT];
 #pragma unroll
@@ -333,10 +384,11 @@ k_knn_home(const KdNode* __restrict__ nodes, int64_t n_nodes, const T* __restric
             }
         }
     }
-    double b = bd[KM - 1];
+    b = bd[KM - 1];
 #pragma unroll
     for (int j = 0; j < KM - 1; j++)
         if (j == kk - 1) b = bd[j];
+    }
     bound0[t] = b;
     // Entry node: on the root-to-home path the query lies on the near side of every plane
     // (all box offsets zero), and a far child whose bound |q - v|^2 exceeds the bound b can
