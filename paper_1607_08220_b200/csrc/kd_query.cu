@@ -1,21 +1,25 @@
 // kd_query.cu -- exact k-nearest-neighbour search (Algorithm 1, local_query.py:72-172).
 //
-// One thread per query; a warp carries 32 queries that the host orders by the
-// leaf they land in, so a warp's traversals stay coherent (same nodes, same
-// buckets -> broadcast loads from L1).  Per query:
-//   * explicit stack of far children with per-dimension box offsets;
-//   * pruning bound = sum of squared offsets evaluated in fp32 with
-//     round-toward-zero steps, which is provably <= the binary64 distance of
-//     every point in the box (monotone rounding), so pruning never loses a
-//     neighbour;
-//   * leaf scan in binary64 with the reference's exact operation order
-//     (core.py:199-228: ascending dimension, no FMA) -> bit-identical keys;
-//   * top-k kept sorted by (sq_dist, point_id) in registers (k <= 32) or as the
-//     reference's bounded max-heap in global scratch (any k);
-//   * tie semantics of the brute-force oracle (pkg/tests/conftest.py:8-18):
-//     admit d < radius while under-full, replace on lexicographic (d, id) when
-//     full, prune only when bound > k-th distance.  (The reference prunes at
-//     bound >= r' and can lose an exact tie with a smaller id: SURVEY §8(a) Q5.)
+// 2-D / 3-D, k(+1) <= 32 (the BASELINE configs): queries are ordered by 32-bit Morton keys
+// (k_qbox, k_morton, radix sort), then two passes --
+//   k_knn_home     thread per query: descent to the home leaf, an upper bound on the k-th
+//                  distance from that bucket (fp32, rounded up, for float trees) and the first
+//                  path node whose far child can matter;
+//   k_knn_persist  persistent warps, one query per lane from a warp-local pool of the sorted
+//                  order: explicit stack of far children with per-dimension fp32 box offsets,
+//                  chunked bucket scans with deferred insertion into a register top-k list.
+// D >= 4: k_knn_wq (warp per query).  k > 32: k_knn (thread per query, the reference's heap).
+// Any depth / the reference's own walk and counters: kd_walk.cu.
+// Common to all of them:
+//   * pruning bound = sum of squared offsets evaluated in fp32 with round-toward-zero steps,
+//     provably <= the binary64 distance of every point in the box (monotone rounding), so
+//     pruning never loses a neighbour;
+//   * leaf scan in binary64 with the reference's exact operation order (core.py:199-228:
+//     ascending dimension, no FMA) -> bit-identical keys;
+//   * tie semantics of the brute-force oracle (pkg/tests/conftest.py:8-18): admit d < radius
+//     while under-full, replace on lexicographic (d, id) when full, prune only when
+//     bound > k-th distance.  (The reference prunes at bound >= r' and can lose an exact tie
+//     with a smaller id: SURVEY §8(a) Q5; KD_KNN_REFERENCE reproduces that walk.)
 #include <cub/cub.cuh>
 
 #include <algorithm>
